@@ -1,0 +1,134 @@
+/*
+ * tessel_b200 — C ABI of the B200-native schedule-search path.
+ *
+ * Drop-in boundary for the reference's decide-kernel seam
+ *   repsched._core.decide   (/root/reference/pkg/src/repsched/_core/__init__.py:23-28,
+ *                            kernel_c.pyx:23-37)
+ * plus the batched repetend-search engine the reference has no equivalent of
+ * (it evaluates one candidate per Python call: completion.py:318-349,
+ * repetend.py:253-328).  Plain pointers and sizes only; no torch types.
+ *
+ * Status codes follow the reference: TSL_UNSAT=0, TSL_SAT=1, TSL_TIMEOUT=2.
+ * Functions returning int use 0 for success and a negative TSL_E* code on
+ * error (message via tsl_last_error(), thread-local).  The library never
+ * falls back to CPU computation: without a CUDA device every compute entry
+ * point fails with TSL_ENODEV.
+ */
+#ifndef TESSEL_B200_H
+#define TESSEL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSL_UNSAT 0
+#define TSL_SAT 1
+#define TSL_TIMEOUT 2
+
+#define TSL_OK 0
+#define TSL_EINVAL -1  /* malformed arguments / value out of kernel range */
+#define TSL_ENODEV -2  /* no CUDA device / driver */
+#define TSL_ECUDA -3   /* CUDA runtime error */
+#define TSL_ERANGE -4  /* size beyond the compiled limits */
+
+/* Maximum items per decide problem, devices per placement, stages per
+ * placement handled by the batched repetend engine. */
+#define TSL_MAX_ITEMS 512
+#define TSL_MAX_DEVICES 64
+#define TSL_MAX_STAGES 64
+
+const char *tsl_last_error(void);
+int tsl_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int tsl_device_count(void);
+/* Bind the calling thread to a CUDA device. */
+int tsl_set_device(int device);
+
+/* ----------------------------------------------------------------------
+ * Single decide problem — replaces repsched._core.decide
+ * (kernel_c.pyx:23-37): lex-first feasible start vector in `order` within
+ * [lo, hi] under difference edges s[dst] >= s[src] + lag (edges: m rows of
+ * (src, dst, lag), row-major), exclusivity between items with intersecting
+ * device masks, per-device running memory <= cap (cap < 0: unconstrained),
+ * node cap `node_budget` (0 = none) and a wall budget `budget_secs`
+ * (<= 0 = none; replaces the absolute `deadline`).  Node counts equal the
+ * reference's.  Writes out_starts[n] on SAT and *out_nodes always.
+ * Returns the status (>= 0) or a negative error code.
+ * ---------------------------------------------------------------------- */
+int tsl_decide(int n, const int64_t *dur, const uint64_t *devmask, const int64_t *mem,
+               const int64_t *edges, int m, const int64_t *order, const int64_t *lo,
+               const int64_t *hi, int ndev, const int64_t *init_mem, int64_t cap,
+               int64_t node_budget, double budget_secs, int64_t *out_starts,
+               int64_t *out_nodes);
+
+/* Batched form: `count` independent problems evaluated concurrently on the
+ * GPU (one per CUDA thread group).  Each problem uses the fields below with
+ * the same meaning as tsl_decide.  status[i], nodes[i] and
+ * starts[i*stride .. +n_i) are written per problem. */
+typedef struct tsl_problem {
+  int n, m, ndev;
+  const int64_t *dur, *mem, *edges, *order, *lo, *hi, *init_mem;
+  const uint64_t *devmask;
+  int64_t cap, node_budget;
+} tsl_problem;
+
+int tsl_decide_batch(int count, const tsl_problem *probs, double budget_secs, int32_t *status,
+                     int64_t *nodes, int64_t *starts, int stride);
+
+/* ----------------------------------------------------------------------
+ * Batched repetend-search engine (replaces the per-candidate loop of
+ * completion.search + repetend.solve_repetend: completion.py:318-349,
+ * repetend.py:65-90, 93-105, 108-190, 253-302).
+ * A placement is K stages on D devices: per-stage time, memory delta and
+ * device mask, plus the dependency pairs (i, j) sorted ascending.
+ * ---------------------------------------------------------------------- */
+typedef struct tsl_engine tsl_engine;
+
+typedef struct tsl_level_stats {
+  int64_t probes;        /* (candidate, period) probes run at this level   */
+  int64_t root_refuted;  /* refuted by root propagation / root checks      */
+  int64_t nodes;         /* DFS nodes (reference node accounting)          */
+  int64_t capped;        /* probes that hit the node cap (TIMEOUT)         */
+  int64_t sat;           /* probes that returned SAT                       */
+} tsl_level_stats;
+
+tsl_engine *tsl_engine_open(int K, int D, const int32_t *dur, const int32_t *mem,
+                            const uint64_t *devmask, int n_deps, const int32_t *deps,
+                            int device);
+void tsl_engine_close(tsl_engine *e);
+
+/* Number of enumerated candidates at n_r (repetend.py:65-90 order, with the
+ * min-index-0 filter).  Fails with TSL_ERANGE beyond 2^63. */
+int tsl_engine_count(tsl_engine *e, int n_r, uint64_t *out_count);
+/* Host-side unranking (global lexicographic rank -> per-stage indices). */
+int tsl_engine_unrank(tsl_engine *e, int n_r, uint64_t rank, int32_t *out_assignment);
+
+/* Stage a window of ranks [r0, r1) at n_r on the device: unrank, entry
+ * memory, memory gate (cap < 0: none).  Returns the number of candidates
+ * that pass the gate in *out_active and, if gate_out is non-NULL, one byte
+ * per rank (1 = passes, 0 = "infeasible"). */
+int tsl_engine_stage(tsl_engine *e, int n_r, uint64_t r0, uint64_t r1, int64_t cap,
+                     int64_t *out_active, uint8_t *gate_out);
+
+/* Probe every still-active candidate of the staged window at `period` with
+ * the reference's per-probe node cap `node_budget` (0 = none).  Candidates
+ * whose window index exceeds `widx_limit` are retired without probing.
+ * SAT candidates are removed from the active set and reported as
+ * (window index, starts[K]) rows in ascending window-index order, up to
+ * max_sat rows (*out_nsat is the true count).  *out_active receives the
+ * number still active. */
+int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap,
+                     int64_t widx_limit, double budget_secs, int64_t max_sat,
+                     int64_t *out_nsat, int64_t *sat_widx, int32_t *sat_starts,
+                     int64_t *out_active, tsl_level_stats *stats);
+
+/* Device time (ms) of the kernels of the last tsl_engine_stage/probe call,
+ * measured with CUDA events on the engine's stream. */
+float tsl_engine_last_kernel_ms(tsl_engine *e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,644 @@
+// tessel_b200.cu — sm_100a kernels and the C ABI (include/tessel_b200.h).
+//
+// Kernels
+//   k_decide_batch  general reference-exact decide, one problem per thread
+//                   (replaces repsched._core.decide, kernel_c.pyx:23-508)
+//   k_stage         K1: unrank a window of candidate ranks in the reference's
+//                   lexicographic order (repetend.py:65-90), entry memory and
+//                   memory gate (repetend.py:93-105, 264-268)
+//   k_probe         K2: one (candidate, period) repetend probe per thread —
+//                   anchored bounds + period-parametric lags
+//                   (repetend.py:160-190) + reference-exact decide; SAT rows
+//                   are compacted out, the rest stay active for the next
+//                   period (the period scan of repetend.py:289-302, run
+//                   level-synchronously across the window)
+// All arithmetic is int32 on the ALU/FMA pipes; no tensor cores, HBM holds
+// only the window's assignments, the active lists and per-thread DFS scratch.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/tessel_b200.h"
+#include "host_build.hpp"
+#include "models.cuh"
+
+#define TSL_VERSION 1
+
+static thread_local std::string g_err;
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw tsl::Error(TSL_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+static int set_err(int code, const std::string &m) {
+  g_err = m;
+  return code;
+}
+
+#define API_BEGIN try {
+#define API_END                                                  \
+  }                                                              \
+  catch (const tsl::Error &e) {                                  \
+    return set_err(e.code, e.what());                            \
+  }                                                              \
+  catch (const std::exception &e) {                              \
+    return set_err(TSL_EINVAL, e.what());                        \
+  }
+
+static void require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw tsl::Error(TSL_ENODEV, std::string("no CUDA device available (") +
+                                     (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                                     "); the B200 path has no CPU fallback");
+  }
+}
+
+// ------------------------------------------------------------------ kernels
+
+__global__ void __launch_bounds__(32) k_decide_batch(const int *__restrict__ pools,
+                                                     const long long *__restrict__ pool_off,
+                                                     int count,
+                                                     const long long *__restrict__ budgets,
+                                                     unsigned long long budget_ns, int *ws_base,
+                                                     const long long *__restrict__ ws_off,
+                                                     int *status, long long *nodes, int *starts,
+                                                     int stride) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int *pool = pools + pool_off[i];
+  const GenView g = gen_view(pool);
+  RxWs w = rx_ws_carve(ws_base + ws_off[i], g.n_, pool[G_MAXDI]);
+  for (int k = 0; k < g.n_; ++k) {
+    w.lo[k] = g.lo_[k];
+    w.hi[k] = g.hi_[k];
+  }
+  const unsigned long long t_end = budget_ns ? rx_now_ns() + budget_ns : 0ull;
+  long long nd = 0;
+  const int st = rx_decide(g, w, budgets[i], t_end, &nd);
+  status[i] = st;
+  nodes[i] = nd;
+  if (st == RX_SAT)
+    for (int k = 0; k < g.n_; ++k) starts[(long long)i * stride + k] = w.s[k];
+}
+
+__device__ __forceinline__ void load_pool(int *sp, const int *__restrict__ gpool) {
+  const int words = gpool[R_WORDS];
+  for (int i = threadIdx.x; i < words; i += blockDim.x) sp[i] = gpool[i];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(128) k_stage(const int *__restrict__ gpool,
+                                               const unsigned long long *__restrict__ cnt,
+                                               const long long *__restrict__ off, int n_r,
+                                               unsigned long long r0, long long W, int cap,
+                                               unsigned char *__restrict__ assign,
+                                               unsigned char *__restrict__ gate, int *act,
+                                               int *n_act) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K], D = sp[R_D];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long wi = (long long)blockIdx.x * blockDim.x + threadIdx.x; wi < W; wi += stride) {
+    unsigned char a[TSL_MAX_STAGES];
+    bool pass = rep_unrank(sp, cnt, off, n_r, r0 + (unsigned long long)wi, a);
+    if (pass && cap >= 0) {
+      // entry memory e_d = sum n_st * m_st over stages on d (repetend.py:93-100)
+      for (int d = 0; d < D && pass; ++d) {
+        int e = 0;
+        for (int p = at_ptr(sp, R_DEVPTR, d); p < at_ptr(sp, R_DEVPTR, d + 1); ++p) {
+          const int st = sp[sp[R_DEVITEMS] + p];
+          e += (int)a[st] * sp[sp[R_MEM] + st];
+        }
+        if (e > cap) pass = false;
+      }
+    }
+    unsigned char *dst = assign + wi * K;
+    for (int st = 0; st < K; ++st) dst[st] = a[st];
+    gate[wi] = pass ? 1 : 0;
+    if (pass) act[atomicAdd(n_act, 1)] = (int)wi;
+  }
+}
+
+// stats layout (u64): probes, root_refuted, nodes, capped, sat
+__global__ void __launch_bounds__(128) k_probe(const int *__restrict__ gpool,
+                                               const unsigned char *__restrict__ assign,
+                                               const int *__restrict__ act_in, int n_in,
+                                               int *act_out, int *counters, int *sat_widx,
+                                               int *sat_starts, int P, long long budget, int cap,
+                                               long long widx_limit,
+                                               unsigned long long budget_ns, int *ws_base,
+                                               long long ws_words,
+                                               unsigned long long *stats) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int *mine = ws_base + tid * ws_words;
+  RxWs w = rx_ws_carve(mine, K, sp[R_MAXDI]);
+  int *coef = mine + rx_ws_words(K, sp[R_MAXDI]);
+  int *init = coef + (sp[R_NDEP] > 0 ? sp[R_NDEP] : 1);
+  unsigned long long s_probe = 0, s_root = 0, s_nodes = 0, s_cap = 0, s_sat = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = tid; t < n_in; t += stride) {
+    const int widx = act_in[t];
+    if (widx > widx_limit) continue;  // retired by a lower-index completion-feasible SAT
+    const unsigned char *a = assign + (long long)widx * K;
+    rep_prepare(sp, a, P, coef, init, w.lo, w.hi);
+    RepView v;
+    v.pool = sp;
+    v.coef = coef;
+    v.init = init;
+    v.P = P;
+    v.cap_ = cap;
+    const unsigned long long t_end = budget_ns ? rx_now_ns() + budget_ns : 0ull;
+    long long nd = 0;
+    const int st = rx_decide(v, w, budget, t_end, &nd);
+    ++s_probe;
+    s_nodes += (unsigned long long)nd;
+    if (st == RX_SAT) {
+      ++s_sat;
+      const int k = atomicAdd(&counters[1], 1);
+      sat_widx[k] = widx;
+      for (int i = 0; i < K; ++i) sat_starts[(long long)k * K + i] = w.s[i];
+    } else {
+      if (st == RX_TIMEOUT) ++s_cap;
+      else if (nd == 0) ++s_root;
+      act_out[atomicAdd(&counters[0], 1)] = widx;
+    }
+  }
+  if (s_probe) {
+    atomicAdd(&stats[0], s_probe);
+    atomicAdd(&stats[1], s_root);
+    atomicAdd(&stats[2], s_nodes);
+    atomicAdd(&stats[3], s_cap);
+    atomicAdd(&stats[4], s_sat);
+  }
+}
+
+// ------------------------------------------------------------------ decide API
+
+namespace {
+
+struct DecideCtx {
+  std::mutex mu;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  char *buf = nullptr;
+  size_t cap = 0;
+
+  char *reserve(size_t bytes) {
+    if (bytes > cap) {
+      if (buf) CK(cudaFree(buf));
+      buf = nullptr;
+      size_t want = std::max(bytes, cap * 2);
+      CK(cudaMalloc(&buf, want));
+      cap = want;
+    }
+    return buf;
+  }
+};
+
+DecideCtx &decide_ctx() {
+  static DecideCtx ctx;
+  return ctx;
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, int32_t *status,
+                      int64_t *nodes, int64_t *starts, int stride) {
+  require_device();
+  if (count <= 0) return;
+  std::vector<int> pools;
+  std::vector<long long> pool_off(count), ws_off(count), budgets(count);
+  long long ws_total = 0;
+  int max_n = 0;
+  for (int i = 0; i < count; ++i) {
+    const tsl_problem &p = probs[i];
+    std::vector<int> one = tsl::gen_build(p.n, p.dur, p.devmask, p.mem, p.edges, p.m, p.order,
+                                          p.lo, p.hi, p.ndev, p.init_mem, p.cap);
+    pool_off[i] = (long long)pools.size();
+    pools.insert(pools.end(), one.begin(), one.end());
+    ws_off[i] = ws_total;
+    ws_total += (rx_ws_words(p.n, one[G_MAXDI]) + 3) / 4 * 4;
+    budgets[i] = p.node_budget < 0 ? 0 : p.node_budget;
+    max_n = std::max(max_n, p.n);
+  }
+  if (stride < max_n) throw tsl::Error(TSL_EINVAL, "starts stride smaller than a problem size");
+  DecideCtx &ctx = decide_ctx();
+  std::lock_guard<std::mutex> lock(ctx.mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (ctx.device != dev) {
+    ctx.device = dev;
+    ctx.stream = nullptr;
+    ctx.buf = nullptr;
+    ctx.cap = 0;
+    CK(cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking));
+  }
+  const size_t b_pool = align_up(pools.size() * sizeof(int));
+  const size_t b_off = align_up(count * sizeof(long long));
+  const size_t b_ws = align_up((size_t)ws_total * sizeof(int));
+  const size_t b_st = align_up(count * sizeof(int));
+  const size_t b_nd = align_up(count * sizeof(long long));
+  const size_t b_starts = align_up((size_t)count * stride * sizeof(int));
+  char *base = ctx.reserve(b_pool + 3 * b_off + b_ws + b_st + b_nd + b_starts);
+  char *q = base;
+  int *d_pools = (int *)q; q += b_pool;
+  long long *d_poff = (long long *)q; q += b_off;
+  long long *d_woff = (long long *)q; q += b_off;
+  long long *d_bud = (long long *)q; q += b_off;
+  int *d_ws = (int *)q; q += b_ws;
+  int *d_st = (int *)q; q += b_st;
+  long long *d_nd = (long long *)q; q += b_nd;
+  int *d_starts = (int *)q;
+  cudaStream_t s = ctx.stream;
+  CK(cudaMemcpyAsync(d_pools, pools.data(), pools.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_poff, pool_off.data(), count * sizeof(long long), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_woff, ws_off.data(), count * sizeof(long long), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_bud, budgets.data(), count * sizeof(long long), cudaMemcpyHostToDevice, s));
+  const unsigned long long budget_ns =
+      budget_secs > 0 ? (unsigned long long)(budget_secs * 1e9) : 0ull;
+  const int threads = 32;
+  k_decide_batch<<<(count + threads - 1) / threads, threads, 0, s>>>(
+      d_pools, d_poff, count, d_bud, budget_ns, d_ws, d_woff, d_st, d_nd, d_starts, stride);
+  CK(cudaGetLastError());
+  std::vector<int> h_st(count);
+  std::vector<long long> h_nd(count);
+  std::vector<int> h_starts((size_t)count * stride);
+  CK(cudaMemcpyAsync(h_st.data(), d_st, count * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h_nd.data(), d_nd, count * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h_starts.data(), d_starts, (size_t)count * stride * sizeof(int),
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < count; ++i) {
+    status[i] = h_st[i];
+    nodes[i] = h_nd[i];
+    if (starts && h_st[i] == RX_SAT)
+      for (int k = 0; k < probs[i].n; ++k)
+        starts[(size_t)i * stride + k] = h_starts[(size_t)i * stride + k];
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ engine
+
+struct tsl_engine {
+  tsl::Placement pl;
+  std::vector<int> pool;
+  int device = 0;
+  bool gpu_ready = false;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  int *d_pool = nullptr;
+  // enumeration tables (host copy per n_r, device copy of the staged n_r)
+  int h_nr = -1;
+  std::vector<unsigned long long> h_cnt;
+  std::vector<long long> h_off;
+  int d_nr = -1;
+  unsigned long long *d_cnt = nullptr;
+  long long *d_off = nullptr;
+  size_t d_cnt_cap = 0, d_off_cap = 0;
+  // staged window
+  long long W = 0, W_cap = 0, n_act = 0;
+  int cur = 0;
+  unsigned char *d_assign = nullptr, *d_gate = nullptr;
+  int *d_act[2] = {nullptr, nullptr};
+  int *d_sat_widx = nullptr, *d_sat_starts = nullptr;
+  int *d_counters = nullptr;
+  unsigned long long *d_stats = nullptr;
+  // per-thread DFS scratch
+  int *d_ws = nullptr;
+  long long ws_words = 0;
+  int ws_threads = 0;
+  int num_sms = 148;
+  size_t smem_bytes = 0;
+
+  void host_tables(int n_r) {
+    if (h_nr == n_r) return;
+    tsl::rep_counts(pool, n_r, h_cnt, h_off);
+    h_nr = n_r;
+  }
+
+  void ensure_gpu() {
+    if (gpu_ready) return;
+    require_device();
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaMalloc(&d_pool, pool.size() * sizeof(int)));
+    CK(cudaMemcpy(d_pool, pool.data(), pool.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&d_counters, 4 * sizeof(int)));
+    CK(cudaMalloc(&d_stats, 8 * sizeof(unsigned long long)));
+    smem_bytes = pool.size() * sizeof(int);
+    if (smem_bytes > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem_bytes));
+      CK(cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem_bytes));
+    }
+    const int K = pool[R_K];
+    const int ndep = pool[R_NDEP];
+    ws_words = rx_ws_words(K, pool[R_MAXDI]) + std::max(ndep, 1) + pool[R_D];
+    ws_words = (ws_words + 31) / 32 * 32;
+    ws_threads = num_sms * 4 * 128;
+    CK(cudaMalloc(&d_ws, (size_t)ws_threads * ws_words * sizeof(int)));
+    gpu_ready = true;
+  }
+
+  void device_tables(int n_r) {
+    if (d_nr == n_r) return;
+    host_tables(n_r);
+    if (h_cnt.size() > d_cnt_cap) {
+      if (d_cnt) CK(cudaFree(d_cnt));
+      CK(cudaMalloc(&d_cnt, h_cnt.size() * sizeof(unsigned long long)));
+      d_cnt_cap = h_cnt.size();
+    }
+    if (h_off.size() > d_off_cap) {
+      if (d_off) CK(cudaFree(d_off));
+      CK(cudaMalloc(&d_off, h_off.size() * sizeof(long long)));
+      d_off_cap = h_off.size();
+    }
+    CK(cudaMemcpy(d_cnt, h_cnt.data(), h_cnt.size() * sizeof(unsigned long long),
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_off, h_off.data(), h_off.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    d_nr = n_r;
+  }
+
+  void ensure_window(long long w) {
+    if (w <= W_cap) return;
+    for (void *p : {(void *)d_assign, (void *)d_gate, (void *)d_act[0], (void *)d_act[1],
+                    (void *)d_sat_widx, (void *)d_sat_starts})
+      if (p) CK(cudaFree(p));
+    const int K = pool[R_K];
+    CK(cudaMalloc(&d_assign, (size_t)w * K));
+    CK(cudaMalloc(&d_gate, (size_t)w));
+    CK(cudaMalloc(&d_act[0], (size_t)w * sizeof(int)));
+    CK(cudaMalloc(&d_act[1], (size_t)w * sizeof(int)));
+    CK(cudaMalloc(&d_sat_widx, (size_t)w * sizeof(int)));
+    CK(cudaMalloc(&d_sat_starts, (size_t)w * K * sizeof(int)));
+    W_cap = w;
+  }
+
+  ~tsl_engine() {
+    if (!gpu_ready) return;
+    for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
+                    (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
+                    (void *)d_counters, (void *)d_stats, (void *)d_ws})
+      if (p) cudaFree(p);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    cudaStreamDestroy(stream);
+  }
+};
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+const char *tsl_last_error(void) { return g_err.c_str(); }
+
+int tsl_version(void) { return TSL_VERSION; }
+
+int tsl_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int tsl_set_device(int device) {
+  API_BEGIN
+  require_device();
+  CK(cudaSetDevice(device));
+  return TSL_OK;
+  API_END
+}
+
+int tsl_decide(int n, const int64_t *dur, const uint64_t *devmask, const int64_t *mem,
+               const int64_t *edges, int m, const int64_t *order, const int64_t *lo,
+               const int64_t *hi, int ndev, const int64_t *init_mem, int64_t cap,
+               int64_t node_budget, double budget_secs, int64_t *out_starts,
+               int64_t *out_nodes) {
+  API_BEGIN
+  tsl_problem p;
+  p.n = n;
+  p.m = m;
+  p.ndev = ndev;
+  p.dur = dur;
+  p.mem = mem;
+  p.edges = edges;
+  p.order = order;
+  p.lo = lo;
+  p.hi = hi;
+  p.init_mem = init_mem;
+  p.devmask = devmask;
+  p.cap = cap;
+  p.node_budget = node_budget;
+  int32_t st = 0;
+  int64_t nd = 0;
+  run_decide_batch(1, &p, budget_secs, &st, &nd, out_starts, std::max(n, 1));
+  if (out_nodes) *out_nodes = nd;
+  return st;
+  API_END
+}
+
+int tsl_decide_batch(int count, const tsl_problem *probs, double budget_secs, int32_t *status,
+                     int64_t *nodes, int64_t *starts, int stride) {
+  API_BEGIN
+  if (count < 0) throw tsl::Error(TSL_EINVAL, "negative problem count");
+  run_decide_batch(count, probs, budget_secs, status, nodes, starts, stride);
+  return TSL_OK;
+  API_END
+}
+
+tsl_engine *tsl_engine_open(int K, int D, const int32_t *dur, const int32_t *mem,
+                            const uint64_t *devmask, int n_deps, const int32_t *deps,
+                            int device) {
+  tsl_engine *e = nullptr;
+  try {
+    for (int i = 0; i < K; ++i) {
+      tsl::ck(dur[i], "dur");
+      tsl::ck(mem[i], "mem");
+      if (dur[i] < 1) throw tsl::Error(TSL_EINVAL, "time_cost must be >= 1");
+    }
+    e = new tsl_engine();
+    e->pl.K = K;
+    e->pl.D = D;
+    e->pl.dur.assign(dur, dur + K);
+    e->pl.mem.assign(mem, mem + K);
+    e->pl.mask.assign(devmask, devmask + K);
+    for (int i = 0; i < n_deps; ++i) {
+      const int a = deps[2 * i], b = deps[2 * i + 1];
+      if (a < 0 || a >= K || b < 0 || b >= K) {
+        delete e;
+        set_err(TSL_EINVAL, "dependency references a missing stage");
+        return nullptr;
+      }
+      e->pl.deps.push_back({a, b});
+    }
+    std::sort(e->pl.deps.begin(), e->pl.deps.end());
+    e->pool = tsl::rep_build(e->pl);
+    e->device = device;
+    return e;
+  } catch (const tsl::Error &err) {
+    delete e;
+    set_err(err.code, err.what());
+    return nullptr;
+  } catch (const std::exception &err) {
+    delete e;
+    set_err(TSL_EINVAL, err.what());
+    return nullptr;
+  }
+}
+
+void tsl_engine_close(tsl_engine *e) { delete e; }
+
+int tsl_engine_count(tsl_engine *e, int n_r, uint64_t *out_count) {
+  API_BEGIN
+  if (n_r < 1) throw tsl::Error(TSL_EINVAL, "n_r must be >= 1");
+  e->host_tables(n_r);
+  const unsigned long long c = e->h_cnt[e->h_off[0] + 0];
+  if (c >= (1ULL << 63)) throw tsl::Error(TSL_ERANGE, "candidate count exceeds 2^63");
+  *out_count = c;
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_unrank(tsl_engine *e, int n_r, uint64_t rank, int32_t *out_assignment) {
+  API_BEGIN
+  e->host_tables(n_r);
+  std::vector<int> av(e->pool[R_K], 0);
+  int *a = av.data();
+  if (!rep_unrank(e->pool.data(), e->h_cnt.data(), e->h_off.data(), n_r, rank, a))
+    throw tsl::Error(TSL_EINVAL, "rank out of range");
+  for (size_t i = 0; i < av.size(); ++i) out_assignment[i] = av[i];
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_stage(tsl_engine *e, int n_r, uint64_t r0, uint64_t r1, int64_t cap,
+                     int64_t *out_active, uint8_t *gate_out) {
+  API_BEGIN
+  if (r1 < r0) throw tsl::Error(TSL_EINVAL, "empty rank window");
+  const long long W = (long long)(r1 - r0);
+  if (W > (1LL << 30)) throw tsl::Error(TSL_ERANGE, "window larger than 2^30 ranks");
+  e->ensure_gpu();
+  CK(cudaSetDevice(e->device));
+  e->device_tables(n_r);
+  e->ensure_window(std::max(W, 1LL));
+  const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
+  CK(cudaMemsetAsync(e->d_counters, 0, 4 * sizeof(int), e->stream));
+  const int threads = 128;
+  long long blocks = (W + threads - 1) / threads;
+  blocks = std::max(1LL, std::min<long long>(blocks, (long long)e->num_sms * 8));
+  CK(cudaEventRecord(e->ev0, e->stream));
+  k_stage<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
+      e->d_pool, e->d_cnt, e->d_off, n_r, r0, W, icap, e->d_assign, e->d_gate, e->d_act[0],
+      e->d_counters);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e->ev1, e->stream));
+  int n_act = 0;
+  CK(cudaMemcpyAsync(&n_act, e->d_counters, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  if (gate_out)
+    CK(cudaMemcpyAsync(gate_out, e->d_gate, (size_t)W, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
+  e->W = W;
+  e->n_act = n_act;
+  e->cur = 0;
+  *out_active = n_act;
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap,
+                     int64_t widx_limit, double budget_secs, int64_t max_sat,
+                     int64_t *out_nsat, int64_t *sat_widx, int32_t *sat_starts,
+                     int64_t *out_active, tsl_level_stats *stats) {
+  API_BEGIN
+  if (!e->gpu_ready) throw tsl::Error(TSL_EINVAL, "tsl_engine_probe before tsl_engine_stage");
+  CK(cudaSetDevice(e->device));
+  const int K = e->pool[R_K];
+  tsl::ck(2LL * (K - 1) * ((long long)period + e->pool[R_MAXDUR]) + 4LL * e->pool[R_TOTAL],
+          "period anchor");
+  const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
+  const long long n_in = e->n_act;
+  CK(cudaMemsetAsync(e->d_counters, 0, 4 * sizeof(int), e->stream));
+  CK(cudaMemsetAsync(e->d_stats, 0, 8 * sizeof(unsigned long long), e->stream));
+  const int threads = 128;
+  long long blocks = (n_in + threads - 1) / threads;
+  blocks = std::max(1LL, std::min<long long>(blocks, (long long)e->ws_threads / threads));
+  const unsigned long long budget_ns =
+      budget_secs > 0 ? (unsigned long long)(budget_secs * 1e9) : 0ull;
+  CK(cudaEventRecord(e->ev0, e->stream));
+  if (n_in > 0) {
+    k_probe<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
+        e->d_pool, e->d_assign, e->d_act[e->cur], (int)n_in, e->d_act[1 - e->cur],
+        e->d_counters, e->d_sat_widx, e->d_sat_starts, period,
+        node_budget < 0 ? 0 : node_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words,
+        e->d_stats);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(e->ev1, e->stream));
+  int counters[4] = {0, 0, 0, 0};
+  unsigned long long st[8] = {0};
+  CK(cudaMemcpyAsync(counters, e->d_counters, 4 * sizeof(int), cudaMemcpyDeviceToHost,
+                     e->stream));
+  CK(cudaMemcpyAsync(st, e->d_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
+  const int n_out = counters[0], n_sat = counters[1];
+  std::vector<int> widx(n_sat), rows((size_t)n_sat * K);
+  if (n_sat > 0) {
+    CK(cudaMemcpyAsync(widx.data(), e->d_sat_widx, n_sat * sizeof(int), cudaMemcpyDeviceToHost,
+                       e->stream));
+    CK(cudaMemcpyAsync(rows.data(), e->d_sat_starts, (size_t)n_sat * K * sizeof(int),
+                       cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  }
+  std::vector<int> perm(n_sat);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::sort(perm.begin(), perm.end(), [&](int x, int y) { return widx[x] < widx[y]; });
+  const long long keep = std::min<long long>(n_sat, max_sat < 0 ? 0 : max_sat);
+  for (long long r = 0; r < keep; ++r) {
+    sat_widx[r] = widx[perm[r]];
+    for (int i = 0; i < K; ++i) sat_starts[r * K + i] = rows[(size_t)perm[r] * K + i];
+  }
+  *out_nsat = n_sat;
+  e->cur = 1 - e->cur;
+  e->n_act = n_out;
+  *out_active = n_out;
+  if (stats) {
+    stats->probes = (int64_t)st[0];
+    stats->root_refuted = (int64_t)st[1];
+    stats->nodes = (int64_t)st[2];
+    stats->capped = (int64_t)st[3];
+    stats->sat = (int64_t)st[4];
+  }
+  return TSL_OK;
+  API_END
+}
+
+float tsl_engine_last_kernel_ms(tsl_engine *e) { return e ? e->last_ms : 0.f; }
+
+}  // extern "C"
