@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark: repetend candidates evaluated/s and time-to-optimal of the
+schedule search (BASELINE.json metric) on the X-shape D=8 1:2 workload
+(BASELINE.json configs[1]) at max_nr=4 — the largest C2
+setting the CPU reference finishes, so every step is checked bit-exactly
+against the reference's golden result.
+
+A step = one full ``completion.search()`` (repetend phase over all
+candidates + warmup/cooldown completion).
+
+  value  candidates / s of device time: candidates evaluated in the step ÷
+         the summed CUDA-event time of the engine's kernels (placement
+         tables resident in HBM).
+  e2e    the same metric through the public API: PlacementSpec (host) in,
+         Schedule (host) out, all host<->device traffic in the timed region;
+         time_to_optimal_s is its per-step wall time.
+
+Multi-GPU (torchrun, --gpus N): replicas — every rank runs the same search
+(sharding by candidate index is the next step), value is the
+sum over ranks, timing is the max over ranks.
+
+``--impl reference`` times the reference's own CPU search (oracle/_ref, the
+unmodified reference package built here; else the oracle port) on the host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+os.environ.setdefault("TESSEL_BUDGET_SECS", "1e9")
+
+BASE = json.loads((ROOT / "BASELINE.json").read_text())
+METRIC = BASE["metric"]
+UNIT = "candidates/s"
+DEFAULT_WORKLOAD = "C2@4"
+GOLDEN = {"C2@4": "C2_4", "C2@3": "C2_3", "C1": "C1", "C3@9": "C3_9", "C5@2": "C5_2",
+          "C5@3": "C5_3", "C4b": "C4b", "C3@12": "C3_12", "C4a@3": "C4a_3", "C4a@4": "C4a_4"}
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0, period=0.2):
+        self.index, self.period = index, period
+        self.rows, self._stop = [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _flush_l2(torch, dev):
+    buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    buf.fill_(1)
+    torch.cuda.synchronize(dev)
+
+
+def _golden(workload):
+    name = GOLDEN.get(workload)
+    path = ROOT / "tests" / "golden" / f"search_{name}.json"
+    return json.loads(path.read_text()) if name and path.exists() else None
+
+
+def _matches(res, doc):
+    if doc is None:
+        return None
+    s = res.schedule
+    return (res.report.best_t_r == doc["best_t_r"]
+            and [[list(a), t] for a, t in res.report.improvements] == doc["improvements"]
+            and len(res.report.candidates) == doc["n_candidates"]
+            and sorted([b.stage, b.mb, t] for b, t in s.entries.items())
+            == doc["schedule"]["entries"]
+            and s.makespan() == doc["schedule"]["makespan"])
+
+
+def reference_search(p, cap, max_nr, budget, jobs):
+    """The reference's own CPU search (oracle/_ref) or, if absent, the oracle
+    port.  Returns (kind, candidates, wall, timed_out)."""
+    import oracle
+
+    ref = oracle.load_reference()
+    if ref is not None:
+        from repsched import completion as RC
+        from repsched import placement as RP
+
+        from paper_2311_15269_b200.placement import placement_to_dict
+
+        rp = RP.placement_from_dict(placement_to_dict(p))
+        t0 = time.perf_counter()
+        res = RC.search(rp, cap, max_nr=max_nr, budget=budget, jobs=jobs)
+        wall = time.perf_counter() - t0
+        return "reference", len(res.report.candidates), wall, res.report.timed_out
+    from oracle import search_port
+
+    res = search_port.search(p, cap, max_nr, time_limit=budget)
+    return "port", res.n_candidates, res.wall, res.schedule is None
+
+
+def run_reference_arm(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    from paper_2311_15269_b200.workloads import WORKLOADS
+
+    w = WORKLOADS[args.workload]
+    p = w.placement()
+    jobs = os.cpu_count() or 1
+    vals, walls, kinds = [], [], set()
+    for i in range(args.warmup + args.steps):
+        kind, n, wall, _ = reference_search(p, w.mem_capacity, w.max_nr, args.ref_sample_secs,
+                                            jobs)
+        kinds.add(kind)
+        if i >= args.warmup:
+            vals.append(n / wall)
+            walls.append(wall)
+    v = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(walls), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {w.note}", "max_nr": w.max_nr,
+                   "mem_capacity": w.mem_capacity,
+                   "sample": f"search() with budget={args.ref_sample_secs}s per step"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": jobs, "kind": kinds.pop(),
+                         "sample": f"reference completion.search(jobs={jobs}) on the host, "
+                                   f"wall budget {args.ref_sample_secs}s per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _roofline(kernel_ms_probe, probes, clocks):
+    """Issue roofline of k_probe: warp instructions per probe from the
+    committed ncu capture × live probes ÷ live kernel time."""
+    prof = ROOT / "profiles" / "inst_counts.json"
+    peaks = {}
+    mp = ROOT / "MEASURED_PEAKS.json"
+    if mp.exists():
+        peaks = json.loads(mp.read_text())
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    peak = 148 * 4 * mhz * 1e6  # warp-instructions / s (4 schedulers per SM)
+    out = {"bound": "issue", "unit": "warp-inst/s", "peak": peak,
+           "peak_basis": f"148 SMs x 4 issue/clk x {mhz} MHz (MEASURED_PEAKS sm_max_mhz)",
+           "achieved": None, "frac": None, "traffic": None}
+    if prof.exists() and kernel_ms_probe > 0:
+        d = json.loads(prof.read_text())
+        ipp = d.get("k_probe", {}).get("warp_inst_per_probe")
+        if ipp:
+            ach = ipp * probes / (kernel_ms_probe / 1e3)
+            out.update(achieved=ach, frac=ach / peak,
+                       traffic=d.get("k_probe", {}).get("dram_bytes_per_launch"),
+                       basis=d.get("basis"))
+    return out
+
+
+def run_b200_arm(args):
+    import torch
+
+    rank, world, local = _env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2311_15269_b200 import _native
+    from paper_2311_15269_b200.completion import search
+    from paper_2311_15269_b200.engine import BatchedRepetendSearch
+    from paper_2311_15269_b200.workloads import WORKLOADS
+
+    _native.build()
+    _native.lib().tsl_set_device(local)
+    w = WORKLOADS[args.workload]
+    p = w.placement()
+    golden = _golden(args.workload)
+
+    eng = BatchedRepetendSearch(p, local)      # placement tables resident in HBM
+    for _ in range(args.warmup):
+        res = search(p, w.mem_capacity, max_nr=w.max_nr, engine=eng)
+    parity = _matches(res, golden) if args.warmup else None
+
+    kernel_ms = 0.0
+    cands = 0
+    walls = []
+    stats = {"probes": 0, "nodes": 0, "capped": 0, "root_refuted": 0, "levels": 0}
+    c0 = _native.counters()
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for _ in range(args.steps):
+            _flush_l2(torch, dev)               # L2 flushed between timed steps
+            e0 = eng.counters.kernel_ms
+            n0 = {k: getattr(eng.counters, k) for k in stats}
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            res = search(p, w.mem_capacity, max_nr=w.max_nr, engine=eng)
+            torch.cuda.synchronize(dev)
+            walls.append(time.perf_counter() - t0)
+            kernel_ms += eng.counters.kernel_ms - e0
+            cands += len(res.report.candidates)
+            for k in stats:
+                stats[k] += getattr(eng.counters, k) - n0[k]
+            ok = _matches(res, golden)
+            parity = ok if parity is None else (parity and ok)
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+    c1 = _native.counters()
+    wall = sum(walls)
+    t_dev = kernel_ms / 1e3
+    if dist:
+        t = torch.tensor([wall, t_dev], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall, t_dev = float(t[0]), float(t[1])
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    launches = c1["launches"] - c0["launches"]
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC,
+        "value": world * cands / t_dev if t_dev > 0 else None,
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {w.note}", "max_nr": w.max_nr,
+                   "mem_capacity": w.mem_capacity, "candidates_per_step": cands // args.steps,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "time_to_optimal_s": wall / args.steps,
+        "parity_vs_reference": parity,
+        "e2e": {"value": world * cands / wall, "unit": UNIT,
+                "h2d_bytes_per_step": (c1["h2d_bytes"] - c0["h2d_bytes"]) // args.steps,
+                "d2h_bytes_per_step": (c1["d2h_bytes"] - c0["d2h_bytes"]) // args.steps},
+        "gpu_launches": launches,
+        "work_per_step": {k: v // args.steps for k, v in stats.items()},
+        "clocks": clocks,
+        "roofline": _roofline(kernel_ms, stats["probes"], clocks),
+    }
+    if not args.no_cpu_baseline:
+        kind, n, cwall, _ = reference_search(p, w.mem_capacity, w.max_nr, args.ref_sample_secs, 1)
+        line["cpu_baseline"] = {"value": n / cwall, "unit": UNIT, "cores": 1, "kind": kind,
+                                "sample": f"{args.workload} search(jobs=1) on the host, wall "
+                                          f"budget {args.ref_sample_secs}s ({n} candidates)"}
+        if golden:
+            line["cpu_baseline"]["reference_time_to_optimal_s_container"] = golden["ref_wall_secs"]
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
+    ap.add_argument("--ref-sample-secs", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

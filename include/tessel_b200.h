@@ -124,6 +124,16 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap
                      int64_t *out_nsat, int64_t *sat_widx, int32_t *sat_starts,
                      int64_t *out_active, tsl_level_stats *stats);
 
+/* Rows [first, first+count) of the last probe's SAT list (ascending window
+ * index): window indices and starts[count*K].  Rows stay on the device until
+ * the next tsl_engine_probe / tsl_engine_stage call. */
+int tsl_engine_sat_rows(tsl_engine *e, int64_t first, int64_t count, int64_t *widx_out,
+                        int32_t *starts_out);
+
+/* Process-wide counters since load: kernel launches issued by this library
+ * and bytes copied host->device / device->host (bench accounting). */
+void tsl_counters(int64_t *launches, int64_t *h2d_bytes, int64_t *d2h_bytes);
+
 /* Device time (ms) of the kernels of the last tsl_engine_stage/probe call,
  * measured with CUDA events on the engine's stream. */
 float tsl_engine_last_kernel_ms(tsl_engine *e);

@@ -32,6 +32,13 @@
 
 static thread_local std::string g_err;
 
+// Process-wide accounting for the bench's gpu_launches / e2e byte counts.
+#include <atomic>
+static std::atomic<long long> g_launches{0}, g_h2d{0}, g_d2h{0};
+#define COUNT_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
+#define COUNT_H2D(b) g_h2d.fetch_add((long long)(b), std::memory_order_relaxed)
+#define COUNT_D2H(b) g_d2h.fetch_add((long long)(b), std::memory_order_relaxed)
+
 #define CK(x)                                                                          \
   do {                                                                                 \
     cudaError_t e_ = (x);                                                              \
@@ -53,6 +60,15 @@ static int set_err(int code, const std::string &m) {
   catch (const std::exception &e) {                              \
     return set_err(TSL_EINVAL, e.what());                        \
   }
+
+static void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  COUNT_H2D(bytes);
+}
+static void d2h(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  COUNT_D2H(bytes);
+}
 
 static void require_device() {
   int n = 0;
@@ -187,6 +203,14 @@ __global__ void __launch_bounds__(128) k_probe(const int *__restrict__ gpool,
   }
 }
 
+__global__ void k_gather_rows(const int *__restrict__ rows, const int *__restrict__ pos, int count,
+                              int K, int *__restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)count * K) return;
+  const int r = (int)(t / K), i = (int)(t % K);
+  out[t] = rows[(long long)pos[r] * K + i];
+}
+
 // ------------------------------------------------------------------ decide API
 
 namespace {
@@ -265,23 +289,23 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
   long long *d_nd = (long long *)q; q += b_nd;
   int *d_starts = (int *)q;
   cudaStream_t s = ctx.stream;
-  CK(cudaMemcpyAsync(d_pools, pools.data(), pools.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d_poff, pool_off.data(), count * sizeof(long long), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d_woff, ws_off.data(), count * sizeof(long long), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d_bud, budgets.data(), count * sizeof(long long), cudaMemcpyHostToDevice, s));
+  h2d(d_pools, pools.data(), pools.size() * sizeof(int), s);
+  h2d(d_poff, pool_off.data(), count * sizeof(long long), s);
+  h2d(d_woff, ws_off.data(), count * sizeof(long long), s);
+  h2d(d_bud, budgets.data(), count * sizeof(long long), s);
   const unsigned long long budget_ns =
       budget_secs > 0 ? (unsigned long long)(budget_secs * 1e9) : 0ull;
   const int threads = 32;
+  COUNT_LAUNCH();
   k_decide_batch<<<(count + threads - 1) / threads, threads, 0, s>>>(
       d_pools, d_poff, count, d_bud, budget_ns, d_ws, d_woff, d_st, d_nd, d_starts, stride);
   CK(cudaGetLastError());
   std::vector<int> h_st(count);
   std::vector<long long> h_nd(count);
   std::vector<int> h_starts((size_t)count * stride);
-  CK(cudaMemcpyAsync(h_st.data(), d_st, count * sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(h_nd.data(), d_nd, count * sizeof(long long), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(h_starts.data(), d_starts, (size_t)count * stride * sizeof(int),
-                     cudaMemcpyDeviceToHost, s));
+  d2h(h_st.data(), d_st, count * sizeof(int), s);
+  d2h(h_nd.data(), d_nd, count * sizeof(long long), s);
+  d2h(h_starts.data(), d_starts, (size_t)count * stride * sizeof(int), s);
   CK(cudaStreamSynchronize(s));
   for (int i = 0; i < count; ++i) {
     status[i] = h_st[i];
@@ -321,6 +345,11 @@ struct tsl_engine {
   int *d_sat_widx = nullptr, *d_sat_starts = nullptr;
   int *d_counters = nullptr;
   unsigned long long *d_stats = nullptr;
+  // SAT rows of the last probe, sorted by window index (host) with their
+  // positions in d_sat_starts; rows are gathered on demand
+  std::vector<int> sat_widx_sorted, sat_pos_sorted;
+  int *d_gather = nullptr;
+  size_t d_gather_cap = 0;
   // per-thread DFS scratch
   int *d_ws = nullptr;
   long long ws_words = 0;
@@ -343,7 +372,8 @@ struct tsl_engine {
     CK(cudaEventCreate(&ev1));
     CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaMalloc(&d_pool, pool.size() * sizeof(int)));
-    CK(cudaMemcpy(d_pool, pool.data(), pool.size() * sizeof(int), cudaMemcpyHostToDevice));
+    h2d(d_pool, pool.data(), pool.size() * sizeof(int), stream);
+    CK(cudaStreamSynchronize(stream));
     CK(cudaMalloc(&d_counters, 4 * sizeof(int)));
     CK(cudaMalloc(&d_stats, 8 * sizeof(unsigned long long)));
     smem_bytes = pool.size() * sizeof(int);
@@ -375,9 +405,9 @@ struct tsl_engine {
       CK(cudaMalloc(&d_off, h_off.size() * sizeof(long long)));
       d_off_cap = h_off.size();
     }
-    CK(cudaMemcpy(d_cnt, h_cnt.data(), h_cnt.size() * sizeof(unsigned long long),
-                  cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(d_off, h_off.data(), h_off.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    h2d(d_cnt, h_cnt.data(), h_cnt.size() * sizeof(unsigned long long), stream);
+    h2d(d_off, h_off.data(), h_off.size() * sizeof(long long), stream);
+    CK(cudaStreamSynchronize(stream));
     d_nr = n_r;
   }
 
@@ -400,7 +430,7 @@ struct tsl_engine {
     if (!gpu_ready) return;
     for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
-                    (void *)d_counters, (void *)d_stats, (void *)d_ws})
+                    (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather})
       if (p) cudaFree(p);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -551,15 +581,16 @@ int tsl_engine_stage(tsl_engine *e, int n_r, uint64_t r0, uint64_t r1, int64_t c
   long long blocks = (W + threads - 1) / threads;
   blocks = std::max(1LL, std::min<long long>(blocks, (long long)e->num_sms * 8));
   CK(cudaEventRecord(e->ev0, e->stream));
+  COUNT_LAUNCH();
   k_stage<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
       e->d_pool, e->d_cnt, e->d_off, n_r, r0, W, icap, e->d_assign, e->d_gate, e->d_act[0],
       e->d_counters);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e->ev1, e->stream));
   int n_act = 0;
-  CK(cudaMemcpyAsync(&n_act, e->d_counters, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  d2h(&n_act, e->d_counters, sizeof(int), e->stream);
   if (gate_out)
-    CK(cudaMemcpyAsync(gate_out, e->d_gate, (size_t)W, cudaMemcpyDeviceToHost, e->stream));
+    d2h(gate_out, e->d_gate, (size_t)W, e->stream);
   CK(cudaStreamSynchronize(e->stream));
   CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
   e->W = W;
@@ -591,6 +622,7 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap
       budget_secs > 0 ? (unsigned long long)(budget_secs * 1e9) : 0ull;
   CK(cudaEventRecord(e->ev0, e->stream));
   if (n_in > 0) {
+    COUNT_LAUNCH();
     k_probe<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
         e->d_pool, e->d_assign, e->d_act[e->cur], (int)n_in, e->d_act[1 - e->cur],
         e->d_counters, e->d_sat_widx, e->d_sat_starts, period,
@@ -601,28 +633,29 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap
   CK(cudaEventRecord(e->ev1, e->stream));
   int counters[4] = {0, 0, 0, 0};
   unsigned long long st[8] = {0};
-  CK(cudaMemcpyAsync(counters, e->d_counters, 4 * sizeof(int), cudaMemcpyDeviceToHost,
-                     e->stream));
-  CK(cudaMemcpyAsync(st, e->d_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                     e->stream));
+  d2h(counters, e->d_counters, 4 * sizeof(int), e->stream);
+  d2h(st, e->d_stats, 8 * sizeof(unsigned long long), e->stream);
   CK(cudaStreamSynchronize(e->stream));
   CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
   const int n_out = counters[0], n_sat = counters[1];
-  std::vector<int> widx(n_sat), rows((size_t)n_sat * K);
+  std::vector<int> widx(n_sat);
   if (n_sat > 0) {
-    CK(cudaMemcpyAsync(widx.data(), e->d_sat_widx, n_sat * sizeof(int), cudaMemcpyDeviceToHost,
-                       e->stream));
-    CK(cudaMemcpyAsync(rows.data(), e->d_sat_starts, (size_t)n_sat * K * sizeof(int),
-                       cudaMemcpyDeviceToHost, e->stream));
+    d2h(widx.data(), e->d_sat_widx, n_sat * sizeof(int), e->stream);
     CK(cudaStreamSynchronize(e->stream));
   }
   std::vector<int> perm(n_sat);
   std::iota(perm.begin(), perm.end(), 0);
   std::sort(perm.begin(), perm.end(), [&](int x, int y) { return widx[x] < widx[y]; });
+  e->sat_widx_sorted.resize(n_sat);
+  e->sat_pos_sorted.resize(n_sat);
+  for (int r = 0; r < n_sat; ++r) {
+    e->sat_widx_sorted[r] = widx[perm[r]];
+    e->sat_pos_sorted[r] = perm[r];
+  }
   const long long keep = std::min<long long>(n_sat, max_sat < 0 ? 0 : max_sat);
-  for (long long r = 0; r < keep; ++r) {
-    sat_widx[r] = widx[perm[r]];
-    for (int i = 0; i < K; ++i) sat_starts[r * K + i] = rows[(size_t)perm[r] * K + i];
+  if (keep > 0) {
+    const int rc = tsl_engine_sat_rows(e, 0, keep, sat_widx, sat_starts);
+    if (rc < 0) return rc;
   }
   *out_nsat = n_sat;
   e->cur = 1 - e->cur;
@@ -637,6 +670,40 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap
   }
   return TSL_OK;
   API_END
+}
+
+int tsl_engine_sat_rows(tsl_engine *e, int64_t first, int64_t count, int64_t *widx_out,
+                        int32_t *starts_out) {
+  API_BEGIN
+  const long long n_sat = (long long)e->sat_widx_sorted.size();
+  if (first < 0 || count < 0 || first + count > n_sat)
+    throw tsl::Error(TSL_EINVAL, "SAT row range out of bounds");
+  if (count == 0) return TSL_OK;
+  const int K = e->pool[R_K];
+  const size_t need = (size_t)count * (K + 1);
+  if (need > e->d_gather_cap) {
+    if (e->d_gather) CK(cudaFree(e->d_gather));
+    CK(cudaMalloc(&e->d_gather, need * sizeof(int)));
+    e->d_gather_cap = need;
+  }
+  int *d_pos = e->d_gather, *d_out = e->d_gather + count;
+  h2d(d_pos, e->sat_pos_sorted.data() + first, count * sizeof(int), e->stream);
+  const long long total = count * K;
+  COUNT_LAUNCH();
+  k_gather_rows<<<(int)((total + 255) / 256), 256, 0, e->stream>>>(e->d_sat_starts, d_pos,
+                                                                    (int)count, K, d_out);
+  CK(cudaGetLastError());
+  d2h(starts_out, d_out, total * sizeof(int), e->stream);
+  CK(cudaStreamSynchronize(e->stream));
+  for (long long r = 0; r < count; ++r) widx_out[r] = e->sat_widx_sorted[first + r];
+  return TSL_OK;
+  API_END
+}
+
+void tsl_counters(int64_t *launches, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+  if (launches) *launches = g_launches.load();
+  if (h2d_bytes) *h2d_bytes = g_h2d.load();
+  if (d2h_bytes) *d2h_bytes = g_d2h.load();
 }
 
 float tsl_engine_last_kernel_ms(tsl_engine *e) { return e ? e->last_ms : 0.f; }

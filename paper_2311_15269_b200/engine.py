@@ -1,0 +1,145 @@
+"""Batched repetend search on the B200 (the hot loop of completion.search).
+
+The reference evaluates candidates one at a time, each with a sequential
+period scan (completion.py:318-349 -> repetend.py:253-302).  Here a WINDOW of
+consecutive candidate ranks is staged on the GPU (unrank + memory gate,
+kernel ``k_stage``) and scanned LEVEL-SYNCHRONOUSLY: at period P every
+still-active candidate of the window is probed in one launch (``k_probe``,
+reference-exact decide with the reference's node caps).  After each level the
+host applies the safe bound rule: the lowest-index
+candidate that is SAT at P and completion-feasible retires every
+higher-index candidate (their sequential bound is <= P).  The window is then
+REPLAYED in index order with the reference's improvement rule
+(completion.py:351-382), so improvements, the chosen repetend and the
+candidate records are exactly the reference's.
+
+Why this is exact: a probe's outcome depends only on (candidate, P, node cap),
+and the cap depends only on whether P is the load bound.  A candidate's
+reference scan covers [lb, opt_seq - 1] and stops at the first SAT; the
+level scan covers a superset of that range for every candidate that can still
+matter, and stops a candidate only when its own first SAT is known or when a
+lower-index completion-feasible SAT y at a period <= P bounds it
+(opt_seq(x) <= p1_y).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native
+from .placement import PlacementSpec
+from .repetend import PROBE_NODES, lower_bound
+
+WINDOW_FIRST = 2048
+WINDOW_GROWTH = 4
+WINDOW_MAX = 1 << 21
+SAT_CHUNK = 256
+
+
+@dataclass
+class EngineCounters:
+    """GPU-side work counters (no reference equivalent beyond SolveStats)."""
+    windows: int = 0
+    levels: int = 0
+    probes: int = 0
+    root_refuted: int = 0
+    nodes: int = 0
+    capped: int = 0
+    sat: int = 0
+    kernel_ms: float = 0.0
+    launches: int = 0
+
+    def add_level(self, st: dict, ms: float):
+        self.levels += 1
+        self.launches += 1
+        self.probes += st["probes"]
+        self.root_refuted += st["root_refuted"]
+        self.nodes += st["nodes"]
+        self.capped += st["capped"]
+        self.sat += st["sat"]
+        self.kernel_ms += ms
+
+
+@dataclass
+class WindowResult:
+    n_r: int
+    r0: int
+    count: int
+    first_sat: dict = field(default_factory=dict)  # widx -> (period, starts)
+    gate: Optional[np.ndarray] = None               # 1 = passes the memory gate
+    timed_out: bool = False
+
+
+class BatchedRepetendSearch:
+    """One placement resident on one GPU."""
+
+    def __init__(self, p: PlacementSpec, device: int = 0):
+        self.p = p
+        k = p.num_stages
+        dur = [p.block(s).time_cost for s in range(k)]
+        mem = [p.block(s).mem_delta for s in range(k)]
+        masks = [sum(1 << d for d in p.block(s).devices) for s in range(k)]
+        self.eng = _native.Engine(dur, mem, masks, sorted(p.deps), p.num_devices, device)
+        self.lb = lower_bound(p)
+        self.total = sum(dur)
+        self.counters = EngineCounters()
+
+    def count(self, n_r: int) -> int:
+        return self.eng.count(n_r)
+
+    def unrank(self, n_r: int, rank: int) -> tuple:
+        return self.eng.unrank(n_r, rank)
+
+    def close(self):
+        self.eng.close()
+
+    def evaluate_window(self, n_r: int, r0: int, r1: int, cap: Optional[int], bound: int,
+                        feasible: Callable[[int, int, int, np.ndarray], bool],
+                        deadline: float = 0.0) -> WindowResult:
+        """Level-synchronous period scan of ranks [r0, r1) at n_r under the
+        sequential bound ``bound`` in force at the window start.
+        ``feasible(n_r, rank, period, starts)`` is the completion check."""
+        res = WindowResult(n_r, r0, r1 - r0)
+        n_act, gate = self.eng.stage(n_r, r0, r1, cap, want_gate=cap is not None)
+        self.counters.windows += 1
+        self.counters.launches += 1
+        self.counters.kernel_ms += self.eng.last_kernel_ms()
+        res.gate = gate
+        limit = res.count - 1
+        top = min(self.total, bound - 1)
+        for period in range(self.lb, top + 1):
+            if n_act == 0:
+                break
+            budget_secs = 0.0
+            if deadline:
+                left = deadline - time.monotonic()
+                if left <= 0:
+                    res.timed_out = True
+                    return res
+                budget_secs = left
+            node_cap = 0 if period == self.lb else PROBE_NODES
+            n_sat, widx, rows, n_act, st = self.eng.probe(period, node_cap, cap, limit,
+                                                          budget_secs, SAT_CHUNK)
+            self.counters.add_level(st, self.eng.last_kernel_ms())
+            if deadline and st["capped"] and time.monotonic() > deadline:
+                res.timed_out = True
+                return res
+            i, start = 0, 0
+            while i < n_sat:
+                if i >= start + len(widx):
+                    start = i
+                    widx, rows = self.eng.sat_rows(i, min(SAT_CHUNK, n_sat - i))
+                j = i - start
+                w = int(widx[j])
+                if w > limit:
+                    break
+                res.first_sat[w] = (period, rows[j].copy())
+                if feasible(n_r, r0 + w, period, rows[j]):
+                    limit = w - 1
+                    break
+                i += 1
+        return res

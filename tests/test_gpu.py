@@ -1,0 +1,202 @@
+"""GPU parity tests (run on a B200 with ``-m gpu``): every compute call goes
+through the in-tree sm_100a library via the C ABI; results are compared
+bit-exactly with the reference's golden fixtures and with the oracle."""
+
+import json
+import os
+import random
+
+import pytest
+
+from conftest import GOLDEN, load_probes, load_search, probe_names
+
+pytestmark = pytest.mark.gpu
+
+SLOW = os.environ.get("TESSEL_SLOW", "0") == "1"
+
+
+def _problem(p):
+    return dict(n=p["n"], dur=p["dur"], devmask=p["devmask"], mem=p["mem"], edges=p["edges"],
+                order=p["order"], lo=p["lo"], hi=p["hi"], ndev=p["ndev"], init_mem=p["init"],
+                cap=p["cap"], node_budget=p["budget"])
+
+
+@pytest.mark.parametrize("name", probe_names())
+def test_decide_batch_matches_reference_probes(gpu, name):
+    """k_decide_batch == reference kernel_c: status, lex-min witness, node
+    count — including 400k-node capped TIMEOUT probes and completion probes."""
+    probes = load_probes(name)
+    got = gpu.decide_batch([_problem(p) for p in probes])
+    for p, (st, s, nodes) in zip(probes, got):
+        assert (st, s, nodes) == (p["status"], p["starts"], p["nodes"]), (name, p["kind"])
+
+
+def test_decide_single_and_core_seam(gpu):
+    from paper_2311_15269_b200 import _core
+
+    assert _core.KERNEL_NAME == "b200"
+    probes = load_probes("C1")[:20]
+    for p in probes:
+        r = _core.decide(p["n"], p["dur"], p["devmask"], p["mem"], p["edges"], p["order"],
+                         p["lo"], p["hi"], p["ndev"], p["init"], p["cap"], p["budget"])
+        assert r == (p["status"], p["starts"], p["nodes"])
+
+
+def test_decide_edge_cases(gpu):
+    import oracle
+
+    cases = [
+        (0, [], [], [], [], [], [], [], 2, [0, 0], -1, 0),          # empty
+        (0, [], [], [], [], [], [], [], 1, [5], 3, 0),              # init > cap, no items
+        (1, [2], [1], [1], [], [0], [0], [0], 1, [0], 0, 0),        # memory cap violated
+        (2, [1, 1], [1, 1], [0, 0], [0, 1, 5, 1, 0, -3], [0, 1], [0, 0], [9, 9], 1, [0], -1, 0),
+        (3, [2, 2, 2], [1, 1, 1], [0, 0, 0], [], [2, 0, 1], [0, 0, 0], [3, 3, 3], 1, [0], -1, 0),
+        (3, [1, 1, 1], [3, 1, 2], [1, -1, 0], [0, 2, 1], [1, 0, 2], [0, 0, 0], [4, 4, 4], 2,
+         [1, 0], 2, 1),                                              # node cap 1
+    ]
+    for c in cases:
+        exp = oracle.decide(*c)
+        got = gpu.decide(*c)
+        assert got == exp, c
+
+
+def test_decide_random_vs_oracle(gpu):
+    import oracle
+
+    rng = random.Random(5)
+    probs, exps = [], []
+    for _ in range(400):
+        n = rng.randint(1, 9)
+        ndev = rng.randint(1, 3)
+        dur = [rng.randint(1, 3) for _ in range(n)]
+        mem = [rng.choice((-1, 0, 1)) for _ in range(n)]
+        mask = [rng.randint(1, (1 << ndev) - 1) for _ in range(n)]
+        edges = []
+        for i in range(n):
+            for j in range(n):
+                if i != j and rng.random() < 0.2:
+                    edges += [i, j, rng.randint(-4, 3)]
+        order = list(range(n))
+        rng.shuffle(order)
+        lo = [rng.randint(0, 3) for _ in range(n)]
+        hi = [v + rng.randint(0, 12) for v in lo]
+        init = [rng.randint(0, 2) for _ in range(ndev)]
+        cap = rng.choice((-1, 2, 3, 5))
+        budget = rng.choice((0, 0, 5, 50))
+        exps.append(oracle.decide(n, dur, mask, mem, edges, order, lo, hi, ndev, init, cap,
+                                  budget))
+        probs.append(dict(n=n, dur=dur, devmask=mask, mem=mem, edges=edges, order=order, lo=lo,
+                          hi=hi, ndev=ndev, init_mem=init, cap=cap, node_budget=budget))
+    assert gpu.decide_batch(probs) == exps
+
+
+def _check(doc, res):
+    assert res.report.best_t_r == doc["best_t_r"]
+    assert [[list(a), t] for a, t in res.report.improvements] == doc["improvements"]
+    assert len(res.report.candidates) == doc["n_candidates"]
+    assert res.report.diagnostics == doc["diagnostics"]
+    s = res.schedule
+    assert sorted([b.stage, b.mb, t] for b, t in s.entries.items()) == doc["schedule"]["entries"]
+    r = s.repetend
+    assert [r.start, r.end, r.period, r.nr] == doc["schedule"]["repetend"]
+    assert s.makespan() == doc["schedule"]["makespan"]
+    counts = dict(res.report.candidates.counts)
+    assert counts == doc["status_counts"]
+    nonbound = [[c.n_r, list(c.assignment), c.t_r, c.status]
+                for c in (res.report.candidates[i] for i in range(len(res.report.candidates)))
+                if c.status != "bound"] if doc["n_candidates"] <= 30000 else None
+    if nonbound is not None:
+        assert nonbound == doc["records"]
+
+
+FAST = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "m4_cap8", "k4_k3", "v2_k4", "nn4_k3",
+        "C1", "C2_3", "C3_9", "C5_2"]
+SLOW_CASES = ["C2_4", "C3_12", "C4a_3", "C4a_4", "C4b", "C5_3"]
+
+
+@pytest.mark.parametrize("name", FAST)
+def test_search_matches_reference(gpu, name):
+    from paper_2311_15269_b200.completion import search
+    from paper_2311_15269_b200.placement import placement_from_dict
+
+    doc = load_search(name)
+    p = placement_from_dict(doc["placement"])
+    _check(doc, search(p, doc["mem_capacity"], max_nr=doc["max_nr"]))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", SLOW_CASES)
+def test_search_matches_reference_full_configs(gpu, name):
+    if not SLOW:
+        pytest.skip("set TESSEL_SLOW=1 for the full-size parity configs")
+    if not (GOLDEN / f"search_{name}.json").exists():
+        pytest.skip("golden not generated")
+    from paper_2311_15269_b200.completion import search
+    from paper_2311_15269_b200.placement import placement_from_dict
+
+    doc = load_search(name)
+    p = placement_from_dict(doc["placement"])
+    _check(doc, search(p, doc["mem_capacity"], max_nr=doc["max_nr"]))
+
+
+def test_search_random_placements(gpu):
+    from paper_2311_15269_b200.completion import NoFeasibleSchedule, search
+    from paper_2311_15269_b200.placement import placement_from_dict
+
+    rows = json.loads((GOLDEN / "search_random.json").read_text())
+    for row in rows:
+        p = placement_from_dict(row["placement"])
+        if row.get("error"):
+            with pytest.raises((NoFeasibleSchedule, ValueError)):
+                search(p, row["mem_capacity"], max_nr=row["max_nr"])
+            continue
+        res = search(p, row["mem_capacity"], max_nr=row["max_nr"])
+        assert res.report.best_t_r == row["best_t_r"]
+        assert [[list(a), t] for a, t in res.report.improvements] == row["improvements"]
+        assert sorted([b.stage, b.mb, t] for b, t in res.schedule.entries.items()) == \
+            row["schedule"]["entries"]
+        assert len(res.report.candidates) == row["n_candidates"]
+
+
+def test_solve_repetend_and_solver_spec_goldens(gpu):
+    """SPEC examples G4, G5, G7, G8, G9 through the single-candidate API."""
+    from paper_2311_15269_b200.completion import cooldown_blocks, warmup_blocks
+    from paper_2311_15269_b200.placement import CostModel, make_shape
+    from paper_2311_15269_b200.repetend import solve_repetend
+    from paper_2311_15269_b200.solver import (SolveRequest, Status, full_request, solve_decide,
+                                              solve_min_makespan)
+
+    v4 = make_shape("vshape", 4, CostModel(1, 2, 1, -1))
+    out = solve_repetend(v4, (3, 2, 1, 0, 0, 0, 0, 0), 4)
+    r = out.repetend
+    assert out.status == "ok" and r.period == 3
+    assert r.internal == (6, 4, 2, 0, 1, 3, 5, 7)
+    assert r.exec_spans == (3, 3, 3, 3) and r.waits == (0, 0, 0, 0)
+    assert len(warmup_blocks(r)) == 6 and len(cooldown_blocks(r)) == 18
+    z = solve_repetend(v4, (0,) * 8, 4).repetend
+    assert z.period == 12 and z.internal == (0, 1, 2, 3, 4, 6, 8, 10)
+    assert solve_min_makespan(full_request(v4, 1)).objective == 12
+    assert solve_min_makespan(full_request(v4, 2)).objective == 15
+    req = full_request(v4, 1, horizon=12, mode="decide")
+    assert solve_decide(req).status == Status.SATISFIABLE
+    req = full_request(v4, 1, horizon=11, mode="decide")
+    assert solve_decide(req).status == Status.INFEASIBLE
+
+
+def test_solve_repetend_matches_oracle(gpu):
+    from oracle import search_port as SP
+    from paper_2311_15269_b200.repetend import solve_repetend
+    from paper_2311_15269_b200.workloads import WORKLOADS
+
+    rng = random.Random(3)
+    for wl in ("C2@3", "C3@9", "C5@2"):
+        w = WORKLOADS[wl]
+        p = w.placement()
+        cands = list(SP.iter_assignments(p, 2))
+        for a in rng.sample(cands, min(8, len(cands))):
+            exp = SP.solve_repetend(p, a, w.mem_capacity, upper=None)
+            got = solve_repetend(p, a, w.mem_capacity)
+            assert got.status == exp.status
+            if exp.status == "ok":
+                assert got.repetend.internal == exp.internal
+                assert got.repetend.period == exp.period
