@@ -92,6 +92,9 @@ typedef struct tsl_level_stats {
   int64_t nodes;         /* DFS nodes (reference node accounting)          */
   int64_t capped;        /* probes that hit the node cap (TIMEOUT)         */
   int64_t sat;           /* probes that returned SAT                       */
+  int64_t deferred;      /* probes over the small budget, sent to resolve   */
+  int64_t dj_refuted;    /* deferred probes proven infeasible by DJ         */
+  int64_t dj_nodes;      /* DJ branching nodes                              */
 } tsl_level_stats;
 
 tsl_engine *tsl_engine_open(int K, int D, const int32_t *dur, const int32_t *mem,
@@ -112,17 +115,34 @@ int tsl_engine_unrank(tsl_engine *e, int n_r, uint64_t rank, int32_t *out_assign
 int tsl_engine_stage(tsl_engine *e, int n_r, uint64_t r0, uint64_t r1, int64_t cap,
                      int64_t *out_active, uint8_t *gate_out);
 
-/* Probe every still-active candidate of the staged window at `period` with
- * the reference's per-probe node cap `node_budget` (0 = none).  Candidates
- * whose window index exceeds `widx_limit` are retired without probing.
- * SAT candidates are removed from the active set and reported as
- * (window index, starts[K]) rows in ascending window-index order, up to
- * max_sat rows (*out_nsat is the true count).  *out_active receives the
- * number still active. */
-int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap,
-                     int64_t widx_limit, double budget_secs, int64_t max_sat,
+/* Probe every still-active candidate of the staged window at `period`.
+ * `node_budget` is the reference's per-probe node cap (0 = none:
+ * repetend.py:289-292).  Each probe first runs the reference-exact DFS with
+ * `small_budget` nodes; probes that exhaust it below the reference cap are
+ * DEFERRED (see tsl_engine_resolve).  Candidates whose window index exceeds
+ * `widx_limit` are retired without probing.  SAT candidates leave the
+ * active set and are reported as (window index, starts[K]) rows in
+ * ascending window-index order, up to max_sat rows (*out_nsat is the true
+ * count).  *out_active / *out_deferred receive the remaining counts. */
+int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t small_budget,
+                     int64_t cap, int64_t widx_limit, double budget_secs, int64_t max_sat,
                      int64_t *out_nsat, int64_t *sat_widx, int32_t *sat_starts,
-                     int64_t *out_active, tsl_level_stats *stats);
+                     int64_t *out_active, int64_t *out_deferred, tsl_level_stats *stats);
+
+/* One stage of settling the deferred probes of the last level whose window
+ * index is <= widx_limit (the others are retired and dropped): when
+ * dj_budget > 0, a complete disjunctive solver first (an infeasibility proof
+ * = "not SAT", the same conclusion the reference draws from its UNSAT or its
+ * node-capped TIMEOUT); then the reference-exact DFS with
+ * min(stage_budget, node_budget) nodes (stage_budget 0 = the reference cap).
+ * Probes exhausting a stage budget below the cap stay deferred for the next
+ * stage.  SAT rows are merged into the level's SAT list (returned sorted as
+ * in tsl_engine_probe); settled non-SAT probes rejoin the active set. */
+int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t stage_budget,
+                       int64_t dj_budget, int64_t cap, int64_t widx_limit, double budget_secs,
+                       int64_t max_sat, int64_t *out_nsat, int64_t *sat_widx,
+                       int32_t *sat_starts, int64_t *out_active, int64_t *out_deferred,
+                       tsl_level_stats *stats);
 
 /* Rows [first, first+count) of the last probe's SAT list (ascending window
  * index): window indices and starts[count*K].  Rows stay on the device until

@@ -63,7 +63,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 class _Stats(ctypes.Structure):
     _fields_ = [("probes", ctypes.c_int64), ("root_refuted", ctypes.c_int64),
-                ("nodes", ctypes.c_int64), ("capped", ctypes.c_int64), ("sat", ctypes.c_int64)]
+                ("nodes", ctypes.c_int64), ("capped", ctypes.c_int64), ("sat", ctypes.c_int64),
+                ("deferred", ctypes.c_int64), ("dj_refuted", ctypes.c_int64),
+                ("dj_nodes", ctypes.c_int64)]
 
 
 class _Problem(ctypes.Structure):
@@ -79,7 +81,8 @@ _lib = None
 EXPORTS = (
     "tsl_last_error", "tsl_version", "tsl_device_count", "tsl_set_device", "tsl_decide",
     "tsl_decide_batch", "tsl_engine_open", "tsl_engine_close", "tsl_engine_count",
-    "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_sat_rows",
+    "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
+    "tsl_engine_sat_rows",
     "tsl_engine_last_kernel_ms", "tsl_counters",
 )
 
@@ -112,7 +115,10 @@ def lib():
     L.tsl_engine_stage.restype = i32
     L.tsl_engine_stage.argtypes = [vp, i32, ctypes.c_uint64, ctypes.c_uint64, i64, vp, vp]
     L.tsl_engine_probe.restype = i32
-    L.tsl_engine_probe.argtypes = [vp, i32, i64, i64, i64, dbl, i64, vp, vp, vp, vp, vp]
+    L.tsl_engine_probe.argtypes = [vp, i32, i64, i64, i64, i64, dbl, i64, vp, vp, vp, vp, vp, vp]
+    L.tsl_engine_resolve.restype = i32
+    L.tsl_engine_resolve.argtypes = [vp, i32, i64, i64, i64, i64, i64, dbl, i64, vp, vp, vp,
+                                     vp, vp, vp]
     L.tsl_engine_sat_rows.restype = i32
     L.tsl_engine_sat_rows.argtypes = [vp, i64, i64, vp, vp]
     L.tsl_counters.restype = None
@@ -254,21 +260,44 @@ class Engine:
                                        _ptr(gate) if gate is not None else None))
         return int(n_act[0]), gate
 
-    def probe(self, period: int, node_budget: int, cap, widx_limit: int, budget_secs=0.0,
-              max_sat=64):
+    def probe(self, period: int, node_budget: int, small_budget: int, cap, widx_limit: int,
+              budget_secs=0.0, max_sat=64):
+        """Level pass -> (n_sat, widx[:k], rows[:k], n_active, n_deferred, stats)."""
         nsat = np.zeros(1, dtype=np.int64)
         n_act = np.zeros(1, dtype=np.int64)
+        n_def = np.zeros(1, dtype=np.int64)
         widx = np.zeros(max(max_sat, 1), dtype=np.int64)
         rows = np.zeros(max(max_sat, 1) * self.K, dtype=np.int32)
         st = _Stats()
-        check(self._L.tsl_engine_probe(self._h, int(period), int(node_budget),
+        check(self._L.tsl_engine_probe(self._h, int(period), int(node_budget), int(small_budget),
                                        -1 if cap is None else int(cap), int(widx_limit),
                                        float(budget_secs), int(max_sat), _ptr(nsat), _ptr(widx),
-                                       _ptr(rows), _ptr(n_act), ctypes.byref(st)))
+                                       _ptr(rows), _ptr(n_act), _ptr(n_def), ctypes.byref(st)))
         n = int(nsat[0])
         k = min(n, max_sat)
         return (n, widx[:k].copy(), rows[:k * self.K].reshape(k, self.K).copy(), int(n_act[0]),
-                {f: getattr(st, f) for f, _ in _Stats._fields_})
+                int(n_def[0]), {f: getattr(st, f) for f, _ in _Stats._fields_})
+
+    def resolve(self, period: int, node_budget: int, stage_budget: int, dj_budget: int, cap,
+                widx_limit: int, budget_secs=0.0, max_sat=64):
+        """One stage of settling deferred probes ->
+        (n_sat, widx[:k], rows[:k], n_active, n_deferred, stats)."""
+        nsat = np.zeros(1, dtype=np.int64)
+        n_act = np.zeros(1, dtype=np.int64)
+        n_def = np.zeros(1, dtype=np.int64)
+        widx = np.zeros(max(max_sat, 1), dtype=np.int64)
+        rows = np.zeros(max(max_sat, 1) * self.K, dtype=np.int32)
+        st = _Stats()
+        check(self._L.tsl_engine_resolve(self._h, int(period), int(node_budget),
+                                         int(stage_budget), int(dj_budget),
+                                         -1 if cap is None else int(cap), int(widx_limit),
+                                         float(budget_secs), int(max_sat), _ptr(nsat),
+                                         _ptr(widx), _ptr(rows), _ptr(n_act), _ptr(n_def),
+                                         ctypes.byref(st)))
+        n = int(nsat[0])
+        k = min(n, max_sat)
+        return (n, widx[:k].copy(), rows[:k * self.K].reshape(k, self.K).copy(), int(n_act[0]),
+                int(n_def[0]), {f: getattr(st, f) for f, _ in _Stats._fields_})
 
     def sat_rows(self, first: int, count: int):
         widx = np.zeros(max(count, 1), dtype=np.int64)

@@ -384,9 +384,7 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
             width = min(width * WINDOW_GROWTH, WINDOW_MAX)
     report.phase_secs["repetend"] += time.monotonic() - t_rep
     c = eng.counters
-    report.engine = {"windows": c.windows, "levels": c.levels, "probes": c.probes,
-                     "root_refuted": c.root_refuted, "nodes": c.nodes, "capped": c.capped,
-                     "sat": c.sat, "kernel_ms": c.kernel_ms, "launches": c.launches}
+    report.engine = dict(c.__dict__)
     report.stats.decides += c.probes
     report.stats.nodes += c.nodes
 

@@ -197,10 +197,39 @@ inline std::vector<int> rep_build(const Placement &pl) {
       in_row[in_ptr[b] + fi[b]++] = r;
     }
   }
-  std::vector<int> conf_ptr(K + 1, 0), conf_dst;
+  std::vector<int> out_dep_end(K), in_dep_end(K), in_srcdur(m);
+  for (int a = 0; a < K; ++a) {
+    int p = out_ptr[a];
+    while (p < out_ptr[a + 1] && out_row[p] < ndep) ++p;
+    out_dep_end[a] = p;
+    p = in_ptr[a];
+    while (p < in_ptr[a + 1] && in_row[p] < ndep) ++p;
+    in_dep_end[a] = p;
+  }
+  for (int p = 0; p < m; ++p) in_srcdur[p] = pl.dur[in_src[p]];
+  // disjunctive pairs {x < y} with intersecting masks
+  std::vector<int> pairx, pairy, pdev_ptr(1, 0), pdev, devnpair(D, 0);
+  std::vector<std::vector<int>> pid(K, std::vector<int>(K, -1));
+  for (int x = 0; x < K; ++x)
+    for (int y = x + 1; y < K; ++y)
+      if (pl.mask[x] & pl.mask[y]) {
+        pid[x][y] = pid[y][x] = (int)pairx.size();
+        pairx.push_back(x);
+        pairy.push_back(y);
+        for (int d = 0; d < D; ++d)
+          if (((pl.mask[x] & pl.mask[y]) >> d) & 1) {
+            pdev.push_back(d);
+            devnpair[d]++;
+          }
+        pdev_ptr.push_back((int)pdev.size());
+      }
+  std::vector<int> conf_ptr(K + 1, 0), conf_dst, conf_pid;
   for (int i = 0; i < K; ++i) {
     for (int j = 0; j < K; ++j)
-      if (i != j && (pl.mask[i] & pl.mask[j])) conf_dst.push_back(j);
+      if (i != j && (pl.mask[i] & pl.mask[j])) {
+        conf_dst.push_back(j);
+        conf_pid.push_back(pid[i][j]);
+      }
     conf_ptr[i + 1] = (int)conf_dst.size();
   }
   std::vector<int> dev_ptr(D + 1, 0), dev_items, devof_ptr(K + 1, 0), devof;
@@ -263,6 +292,7 @@ inline std::vector<int> rep_build(const Placement &pl) {
   pool[R_LB] = lb;
   pool[R_TOTAL] = total;
   pool[R_MAXDI] = maxdi;
+  pool[R_NPAIR] = (int)pairx.size();
   auto put = [&](int slot, const std::vector<int> &v) {
     pool[slot] = (int)pool.size();
     pool.insert(pool.end(), v.begin(), v.end());
@@ -274,18 +304,27 @@ inline std::vector<int> rep_build(const Placement &pl) {
   put(R_OUTPTR, out_ptr);
   put(R_OUTDST, out_dst);
   put(R_OUTROW, out_row);
+  put(R_OUTDEPEND, out_dep_end);
   put(R_INPTR, in_ptr);
   put(R_INSRC, in_src);
   put(R_INROW, in_row);
+  put(R_INDEPEND, in_dep_end);
+  put(R_INSRCDUR, in_srcdur);
   put(R_RBASE, rbase);
   put(R_RSRC, rsrc);
   put(R_RDST, rdst);
   put(R_CONFPTR, conf_ptr);
   put(R_CONFDST, conf_dst);
+  put(R_CONFPID, conf_pid);
   put(R_DEVPTR, dev_ptr);
   put(R_DEVITEMS, dev_items);
   put(R_DEVOFPTR, devof_ptr);
   put(R_DEVOF, devof);
+  put(R_PAIRX, pairx);
+  put(R_PAIRY, pairy);
+  put(R_PDEVPTR, pdev_ptr);
+  put(R_PDEV, pdev);
+  put(R_DEVNPAIR, devnpair);
   put(R_LSPTR, ls_ptr);
   put(R_LS, ls);
   put(R_HSPTR, hs_ptr);

@@ -32,6 +32,13 @@ struct GenView {
   RX_HD int out_end(int a) const { return out_ptr_[a + 1]; }
   RX_HD int out_dst(int p) const { return out_dst_[p]; }
   RX_HD int out_lag(int p) const { return out_lag_[p]; }
+  // every general edge is treated as a "dependency" edge with a stored lag
+  RX_HD int out_dep_end(int a) const { return out_ptr_[a + 1]; }
+  RX_HD int out_dep_lag(int p) const { return out_lag_[p]; }
+  RX_HD int out_win_lag(int) const { return 0; }
+  RX_HD int in_dep_end(int a) const { return in_ptr_[a + 1]; }
+  RX_HD int in_dep_lag(int p) const { return in_lag_[p]; }
+  RX_HD int in_win_lag(int) const { return 0; }
   RX_HD int in_begin(int a) const { return in_ptr_[a]; }
   RX_HD int in_end(int a) const { return in_ptr_[a + 1]; }
   RX_HD int in_src(int p) const { return in_src_[p]; }
@@ -80,60 +87,103 @@ RX_HD GenView gen_view(const int *pool) {
 // Placement structure pool: header ints followed by the arrays; offsets in
 // the header are relative to the pool start.
 enum {
-  R_K = 0, R_D, R_NDEP, R_M, R_MAXDUR, R_LB, R_TOTAL, R_MAXDI,
-  R_DUR, R_MEM, R_ORDER, R_OUTPTR, R_OUTDST, R_OUTROW, R_INPTR, R_INSRC, R_INROW,
-  R_RBASE, R_RSRC, R_RDST, R_CONFPTR, R_CONFDST, R_DEVPTR, R_DEVITEMS, R_DEVOFPTR, R_DEVOF,
+  R_K = 0, R_D, R_NDEP, R_M, R_MAXDUR, R_LB, R_TOTAL, R_MAXDI, R_NPAIR,
+  R_DUR, R_MEM, R_ORDER, R_OUTPTR, R_OUTDST, R_OUTROW, R_OUTDEPEND, R_INPTR, R_INSRC, R_INROW,
+  R_INDEPEND, R_INSRCDUR,
+  R_RBASE, R_RSRC, R_RDST, R_CONFPTR, R_CONFDST, R_CONFPID, R_DEVPTR, R_DEVITEMS, R_DEVOFPTR,
+  R_DEVOF,
+  // disjunctive pairs {x < y} of items with intersecting device masks, the
+  // devices each pair shares, and the number of pairs per device
+  R_PAIRX, R_PAIRY, R_PDEVPTR, R_PDEV, R_DEVNPAIR,
   // enumeration metadata: per stage st, lo sources (succ j < st), hi
   // sources (pred i < st), and the frontier F_{st+1} after assigning st
   R_LSPTR, R_LS, R_HSPTR, R_HS, R_FRPTR, R_FR,
   R_WORDS, R_HDR
 };
 
+// Edge rows are (sorted dependency rows) ++ (device-window rows), and the
+// CSRs keep row order, so every node's out-list (in-list) starts with its
+// dependency entries.  Window rows x->y carry lag t_x - P (coef 1), so the
+// window part needs no per-candidate data: out-lag = dur[a] - P for the
+// popped node a, in-lag = dur[src] - P (stored per in-entry as srcdur).
 struct RepView {
-  const int *pool;
-  const int *coef;  // dependency-row coefficients a[src] - a[dst]
-  const int *init;  // entry memory per device
-  int P, cap_;
+  const int *dur_, *mem_, *order_, *out_ptr_, *out_dst_, *out_row_, *out_dep_end_;
+  const int *in_ptr_, *in_src_, *in_row_, *in_dep_end_, *in_srcdur_;
+  const int *conf_ptr_, *conf_dst_, *dev_ptr_, *dev_items_, *devof_ptr_, *devof_;
+  const int *deplag;  // per dependency row: base - (a[src] - a[dst]) * P
+  const int *init;    // entry memory per device
+  int K, D, P, cap_;
 
-  RX_HD int at(int off, int i) const { return pool[pool[off] + i]; }
-  RX_HD int n() const { return pool[R_K]; }
-  RX_HD int ndev() const { return pool[R_D]; }
+  RX_HD int n() const { return K; }
+  RX_HD int ndev() const { return D; }
   RX_HD int cap() const { return cap_; }
-  RX_HD int dur(int i) const { return at(R_DUR, i); }
-  RX_HD int mem(int i) const { return at(R_MEM, i); }
-  RX_HD int order(int k) const { return at(R_ORDER, k); }
+  RX_HD int dur(int i) const { return dur_[i]; }
+  RX_HD int mem(int i) const { return mem_[i]; }
+  RX_HD int order(int k) const { return order_[k]; }
   RX_HD int init_mem(int d) const { return init[d]; }
-  RX_HD int lag_of_row(int r) const {
-    const int c = r < pool[R_NDEP] ? coef[r] : 1;
-    return at(R_RBASE, r) - c * P;
-  }
-  RX_HD int out_begin(int a) const { return at(R_OUTPTR, a); }
-  RX_HD int out_end(int a) const { return at(R_OUTPTR, a + 1); }
-  RX_HD int out_dst(int p) const { return at(R_OUTDST, p); }
-  RX_HD int out_lag(int p) const { return lag_of_row(at(R_OUTROW, p)); }
-  RX_HD int in_begin(int a) const { return at(R_INPTR, a); }
-  RX_HD int in_end(int a) const { return at(R_INPTR, a + 1); }
-  RX_HD int in_src(int p) const { return at(R_INSRC, p); }
-  RX_HD int in_lag(int p) const { return lag_of_row(at(R_INROW, p)); }
-  RX_HD int conf_begin(int x) const { return at(R_CONFPTR, x); }
-  RX_HD int conf_end(int x) const { return at(R_CONFPTR, x + 1); }
-  RX_HD int conf_dst(int p) const { return at(R_CONFDST, p); }
-  RX_HD int dev_begin(int d) const { return at(R_DEVPTR, d); }
-  RX_HD int dev_end(int d) const { return at(R_DEVPTR, d + 1); }
-  RX_HD int dev_item(int p) const { return at(R_DEVITEMS, p); }
-  RX_HD int devof_begin(int i) const { return at(R_DEVOFPTR, i); }
-  RX_HD int devof_end(int i) const { return at(R_DEVOFPTR, i + 1); }
-  RX_HD int devof(int p) const { return at(R_DEVOF, p); }
+  RX_HD int out_begin(int a) const { return out_ptr_[a]; }
+  RX_HD int out_end(int a) const { return out_ptr_[a + 1]; }
+  RX_HD int out_dst(int p) const { return out_dst_[p]; }
+  RX_HD int out_dep_end(int a) const { return out_dep_end_[a]; }
+  RX_HD int out_dep_lag(int p) const { return deplag[out_row_[p]]; }
+  RX_HD int out_win_lag(int a) const { return dur_[a] - P; }
+  RX_HD int in_begin(int a) const { return in_ptr_[a]; }
+  RX_HD int in_end(int a) const { return in_ptr_[a + 1]; }
+  RX_HD int in_src(int p) const { return in_src_[p]; }
+  RX_HD int in_dep_end(int a) const { return in_dep_end_[a]; }
+  RX_HD int in_dep_lag(int p) const { return deplag[in_row_[p]]; }
+  RX_HD int in_win_lag(int p) const { return in_srcdur_[p] - P; }
+  RX_HD int conf_begin(int x) const { return conf_ptr_[x]; }
+  RX_HD int conf_end(int x) const { return conf_ptr_[x + 1]; }
+  RX_HD int conf_dst(int p) const { return conf_dst_[p]; }
+  RX_HD int dev_begin(int d) const { return dev_ptr_[d]; }
+  RX_HD int dev_end(int d) const { return dev_ptr_[d + 1]; }
+  RX_HD int dev_item(int p) const { return dev_items_[p]; }
+  RX_HD int devof_begin(int i) const { return devof_ptr_[i]; }
+  RX_HD int devof_end(int i) const { return devof_ptr_[i + 1]; }
+  RX_HD int devof(int p) const { return devof_[p]; }
 };
 
+RX_HD RepView rep_view(const int *pool, int P, int cap, const int *deplag, const int *init) {
+  RepView v;
+  v.K = pool[R_K];
+  v.D = pool[R_D];
+  v.P = P;
+  v.cap_ = cap;
+  v.deplag = deplag;
+  v.init = init;
+  v.dur_ = pool + pool[R_DUR];
+  v.mem_ = pool + pool[R_MEM];
+  v.order_ = pool + pool[R_ORDER];
+  v.out_ptr_ = pool + pool[R_OUTPTR];
+  v.out_dst_ = pool + pool[R_OUTDST];
+  v.out_row_ = pool + pool[R_OUTROW];
+  v.out_dep_end_ = pool + pool[R_OUTDEPEND];
+  v.in_ptr_ = pool + pool[R_INPTR];
+  v.in_src_ = pool + pool[R_INSRC];
+  v.in_row_ = pool + pool[R_INROW];
+  v.in_dep_end_ = pool + pool[R_INDEPEND];
+  v.in_srcdur_ = pool + pool[R_INSRCDUR];
+  v.conf_ptr_ = pool + pool[R_CONFPTR];
+  v.conf_dst_ = pool + pool[R_CONFDST];
+  v.dev_ptr_ = pool + pool[R_DEVPTR];
+  v.dev_items_ = pool + pool[R_DEVITEMS];
+  v.devof_ptr_ = pool + pool[R_DEVOFPTR];
+  v.devof_ = pool + pool[R_DEVOF];
+  return v;
+}
+
 // Prepare a repetend probe for assignment a[K] at period P: dependency-row
-// coefficients, entry memory (repetend.py:93-100) and the anchored bounds
-// s_0 = A, s_i in [0, 2A], A = (K-1)(P + max t) (repetend.py:166-169).
+// lags base - (a[src] - a[dst]) * P, entry memory (repetend.py:93-100) and
+// the anchored bounds s_0 = A, s_i in [0, 2A], A = (K-1)(P + max t)
+// (repetend.py:162-169).
 template <class A>
-RX_HD void rep_prepare(const int *pool, const A &a, int P, int *coef, int *init, int *lo, int *hi) {
+RX_HD void rep_prepare(const int *pool, const A &a, int P, int *deplag, int *init, int *lo,
+                       int *hi) {
   const int K = pool[R_K], D = pool[R_D], ndep = pool[R_NDEP];
   for (int r = 0; r < ndep; ++r)
-    coef[r] = (int)a[pool[pool[R_RSRC] + r]] - (int)a[pool[pool[R_RDST] + r]];
+    deplag[r] = pool[pool[R_RBASE] + r] -
+                ((int)a[pool[pool[R_RSRC] + r]] - (int)a[pool[pool[R_RDST] + r]]) * P;
   for (int d = 0; d < D; ++d) init[d] = 0;
   for (int st = 0; st < K; ++st) {
     const int mst = pool[pool[R_MEM] + st] * (int)a[st];

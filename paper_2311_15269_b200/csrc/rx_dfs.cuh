@@ -218,10 +218,10 @@ RX_HD bool rx_propagate(const M &md, RxWs &w, int &qh, int &qt, int &qc, unsigne
     --qc;
     w.inq[a] = 0;
     const int la = w.lo[a], ha = w.hi[a];
-    const int oe = md.out_end(a);
+    const int oe = md.out_end(a), od = md.out_dep_end(a), owl = md.out_win_lag(a);
     for (int p = md.out_begin(a); p < oe; ++p) {
       const int b = md.out_dst(p);
-      const int nl = la + md.out_lag(p);
+      const int nl = la + (p < od ? md.out_dep_lag(p) : owl);
       if (nl > w.lo[b]) {
         if (nl > w.hi[b]) return false;
         if (LOG) rx_save(w, b, ep, tn);
@@ -229,10 +229,10 @@ RX_HD bool rx_propagate(const M &md, RxWs &w, int &qh, int &qt, int &qc, unsigne
         if (!w.inq[b]) rx_push(w, b, n, qt, qc);
       }
     }
-    const int ie = md.in_end(a);
+    const int ie = md.in_end(a), id = md.in_dep_end(a);
     for (int p = md.in_begin(a); p < ie; ++p) {
       const int b = md.in_src(p);
-      const int nh = ha - md.in_lag(p);
+      const int nh = ha - (p < id ? md.in_dep_lag(p) : md.in_win_lag(p));
       if (nh < w.hi[b]) {
         if (nh < w.lo[b]) return false;
         if (LOG) rx_save(w, b, ep, tn);

@@ -27,8 +27,10 @@
 #include "../../include/tessel_b200.h"
 #include "host_build.hpp"
 #include "models.cuh"
+#include "dj_solve.cuh"
+#include "wrx_dfs.cuh"
 
-#define TSL_VERSION 1
+#define TSL_VERSION 2
 
 static thread_local std::string g_err;
 
@@ -109,6 +111,40 @@ __global__ void __launch_bounds__(32) k_decide_batch(const int *__restrict__ poo
     for (int k = 0; k < g.n_; ++k) starts[(long long)i * stride + k] = w.s[k];
 }
 
+// Warp-per-problem variant: lanes cooperate on one reference-exact DFS
+// (wrx_dfs.cuh); mutable state in shared memory (fast shared atomics),
+// per-depth snapshots in global memory.
+__global__ void __launch_bounds__(32) k_decide_warp(const int *__restrict__ pools,
+                                                    const long long *__restrict__ pool_off,
+                                                    int count,
+                                                    const long long *__restrict__ budgets,
+                                                    unsigned long long budget_ns, int *ws_base,
+                                                    const long long *__restrict__ ws_off,
+                                                    int *status, long long *nodes, int *starts,
+                                                    int stride) {
+  extern __shared__ int sm[];
+  const int i = blockIdx.x;
+  if (i >= count) return;
+  const int lane = threadIdx.x & 31;
+  const int *pool = pools + pool_off[i];
+  const GenView g = gen_view(pool);
+  WWs w = wrx_carve(sm, ws_base + ws_off[i], g.n_, pool[G_MAXDI]);
+  for (int k = lane; k < g.n_; k += 32) {
+    w.lo[k] = g.lo_[k];
+    w.hi[k] = g.hi_[k];
+  }
+  __syncwarp();
+  const unsigned long long t_end = budget_ns ? rx_now_ns() + budget_ns : 0ull;
+  long long nd = 0;
+  const int st = wrx_decide(g, w, budgets[i], t_end, &nd);
+  if (lane == 0) {
+    status[i] = st;
+    nodes[i] = nd;
+  }
+  if (st == RX_SAT)
+    for (int k = lane; k < g.n_; k += 32) starts[(long long)i * stride + k] = w.s[k];
+}
+
 __device__ __forceinline__ void load_pool(int *sp, const int *__restrict__ gpool) {
   const int words = gpool[R_WORDS];
   for (int i = threadIdx.x; i < words; i += blockDim.x) sp[i] = gpool[i];
@@ -147,59 +183,248 @@ __global__ void __launch_bounds__(128) k_stage(const int *__restrict__ gpool,
   }
 }
 
-// stats layout (u64): probes, root_refuted, nodes, capped, sat
+// Per-thread scratch of the repetend kernels: RX-DFS or DJ workspace (they
+// run one after the other), then dependency-row lags and entry memory.
+__host__ __device__ inline long long rep_ws_words(const int *pool) {
+  const long long rx = rx_ws_words(pool[R_K], pool[R_MAXDI]);
+  const long long dj = dj_ws_words(pool[R_K], pool[R_D], pool[R_NPAIR], pool[R_MAXDI]);
+  long long w = (rx > dj ? rx : dj) + (pool[R_NDEP] > 0 ? pool[R_NDEP] : 1) + pool[R_D];
+  return (w + 31) / 32 * 32;
+}
+
+struct ProbeOut {
+  int *act_out, *def_out, *sat_widx, *sat_starts;
+  int *counters;  // [0] active, [1] sat, [2] deferred
+  unsigned long long *stats;  // probes, root_refuted, nodes, capped, sat, deferred, dj_unsat, dj_nodes
+};
+
+__device__ __forceinline__ void emit_sat(const ProbeOut &o, int widx, const int *s, int K) {
+  const int k = atomicAdd(&o.counters[1], 1);
+  o.sat_widx[k] = widx;
+  for (int i = 0; i < K; ++i) o.sat_starts[(long long)k * K + i] = s[i];
+}
+
+// K2 level pass: probe (candidate, P) with a small node budget first.
+// Outcomes: SAT (exact: found within the small budget <= the reference cap),
+// UNSAT / TIMEOUT at the reference cap (exact "not SAT"), or DEFERRED (small
+// budget exhausted below the reference cap; settled by k_resolve only if the
+// candidate is still below the level's retirement limit).
 __global__ void __launch_bounds__(128) k_probe(const int *__restrict__ gpool,
                                                const unsigned char *__restrict__ assign,
                                                const int *__restrict__ act_in, int n_in,
-                                               int *act_out, int *counters, int *sat_widx,
-                                               int *sat_starts, int P, long long budget, int cap,
+                                               ProbeOut o, int P, long long full_budget,
+                                               long long small_budget, int cap,
                                                long long widx_limit,
                                                unsigned long long budget_ns, int *ws_base,
-                                               long long ws_words,
-                                               unsigned long long *stats) {
+                                               long long ws_words) {
   extern __shared__ int sp[];
   load_pool(sp, gpool);
   const int K = sp[R_K];
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   int *mine = ws_base + tid * ws_words;
   RxWs w = rx_ws_carve(mine, K, sp[R_MAXDI]);
-  int *coef = mine + rx_ws_words(K, sp[R_MAXDI]);
-  int *init = coef + (sp[R_NDEP] > 0 ? sp[R_NDEP] : 1);
-  unsigned long long s_probe = 0, s_root = 0, s_nodes = 0, s_cap = 0, s_sat = 0;
+  int *deplag = mine + (ws_words - (sp[R_NDEP] > 0 ? sp[R_NDEP] : 1) - sp[R_D]);
+  int *init = deplag + (sp[R_NDEP] > 0 ? sp[R_NDEP] : 1);
+  // a probe is deferred only when the small budget is strictly below the cap
+  const long long first_budget =
+      (full_budget == 0 || small_budget < full_budget) ? small_budget : full_budget;
+  unsigned long long s_probe = 0, s_root = 0, s_nodes = 0, s_cap = 0, s_sat = 0, s_def = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long t = tid; t < n_in; t += stride) {
     const int widx = act_in[t];
     if (widx > widx_limit) continue;  // retired by a lower-index completion-feasible SAT
     const unsigned char *a = assign + (long long)widx * K;
-    rep_prepare(sp, a, P, coef, init, w.lo, w.hi);
-    RepView v;
-    v.pool = sp;
-    v.coef = coef;
-    v.init = init;
-    v.P = P;
-    v.cap_ = cap;
+    rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
+    const RepView v = rep_view(sp, P, cap, deplag, init);
     const unsigned long long t_end = budget_ns ? rx_now_ns() + budget_ns : 0ull;
     long long nd = 0;
-    const int st = rx_decide(v, w, budget, t_end, &nd);
+    const int st = rx_decide(v, w, first_budget, t_end, &nd);
     ++s_probe;
-    s_nodes += (unsigned long long)nd;
     if (st == RX_SAT) {
+      s_nodes += (unsigned long long)nd;
       ++s_sat;
-      const int k = atomicAdd(&counters[1], 1);
-      sat_widx[k] = widx;
-      for (int i = 0; i < K; ++i) sat_starts[(long long)k * K + i] = w.s[i];
+      emit_sat(o, widx, w.s, K);
+    } else if (st == RX_TIMEOUT && first_budget != full_budget) {
+      ++s_def;  // node count settled in k_resolve
+      o.def_out[atomicAdd(&o.counters[2], 1)] = widx;
     } else {
+      s_nodes += (unsigned long long)nd;
       if (st == RX_TIMEOUT) ++s_cap;
       else if (nd == 0) ++s_root;
-      act_out[atomicAdd(&counters[0], 1)] = widx;
+      o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
     }
   }
   if (s_probe) {
-    atomicAdd(&stats[0], s_probe);
-    atomicAdd(&stats[1], s_root);
-    atomicAdd(&stats[2], s_nodes);
-    atomicAdd(&stats[3], s_cap);
-    atomicAdd(&stats[4], s_sat);
+    atomicAdd(&o.stats[0], s_probe);
+    atomicAdd(&o.stats[1], s_root);
+    atomicAdd(&o.stats[2], s_nodes);
+    atomicAdd(&o.stats[3], s_cap);
+    atomicAdd(&o.stats[4], s_sat);
+    atomicAdd(&o.stats[5], s_def);
+  }
+}
+
+// K2 resolution of deferred probes, in escalating stages so that a probe
+// above the level's retirement limit never burns the full reference cap:
+// the complete disjunctive solver first (an infeasibility proof settles the
+// probe as "not SAT", which is what the reference concludes from either its
+// UNSAT or its node-capped TIMEOUT); otherwise the reference-exact RX-DFS
+// with this stage's budget.  Probes exhausting a stage budget below the
+// reference cap are deferred again (def_out) for the next stage.
+__global__ void __launch_bounds__(128) k_resolve(const int *__restrict__ gpool,
+                                                 const unsigned char *__restrict__ assign,
+                                                 const int *__restrict__ def_in, int n_def,
+                                                 ProbeOut o, int P, long long full_budget,
+                                                 long long stage_budget, long long dj_budget,
+                                                 int cap,
+                                                 long long widx_limit,
+                                                 unsigned long long budget_ns, int *ws_base,
+                                                 long long ws_words) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int *mine = ws_base + tid * ws_words;
+  RxWs w = rx_ws_carve(mine, K, sp[R_MAXDI]);
+  DjWs dw = dj_ws_carve(mine, K, sp[R_D], sp[R_NPAIR], sp[R_MAXDI]);
+  int *deplag = mine + (ws_words - (sp[R_NDEP] > 0 ? sp[R_NDEP] : 1) - sp[R_D]);
+  int *init = deplag + (sp[R_NDEP] > 0 ? sp[R_NDEP] : 1);
+  unsigned long long s_nodes = 0, s_cap = 0, s_sat = 0, s_dju = 0, s_djn = 0, s_def = 0;
+  const bool partial = stage_budget > 0 && (full_budget == 0 || stage_budget < full_budget);
+  const long long rx_budget = partial ? stage_budget : full_budget;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = tid; t < n_def; t += stride) {
+    const int widx = def_in[t];
+    if (widx > widx_limit) continue;  // retired meanwhile: never needed
+    const unsigned char *a = assign + (long long)widx * K;
+    const unsigned long long t_end = budget_ns ? rx_now_ns() + budget_ns : 0ull;
+    rep_prepare(sp, a, P, deplag, init, dw.lo, dw.hi);
+    const RepView v = rep_view(sp, P, cap, deplag, init);
+    long long dn = 0;
+    const int dj = dj_budget > 0 ? dj_decide(v, sp, dw, dj_budget, &dn) : DJ_UNKNOWN;
+    s_djn += (unsigned long long)dn;
+    if (dj == DJ_UNSAT) {
+      ++s_dju;
+      o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
+      continue;
+    }
+    rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
+    long long nd = 0;
+    const int st = rx_decide(v, w, rx_budget, t_end, &nd);
+    if (st == RX_SAT) {
+      s_nodes += (unsigned long long)nd;
+      ++s_sat;
+      emit_sat(o, widx, w.s, K);
+    } else if (st == RX_TIMEOUT && partial) {
+      ++s_def;
+      o.def_out[atomicAdd(&o.counters[2], 1)] = widx;
+    } else {
+      s_nodes += (unsigned long long)nd;
+      if (st == RX_TIMEOUT) ++s_cap;
+      o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
+    }
+  }
+  atomicAdd(&o.stats[5], s_def);
+  atomicAdd(&o.stats[2], s_nodes);
+  atomicAdd(&o.stats[3], s_cap);
+  atomicAdd(&o.stats[4], s_sat);
+  atomicAdd(&o.stats[6], s_dju);
+  atomicAdd(&o.stats[7], s_djn);
+}
+
+// Warp-per-probe resolution stage (same contract as k_resolve): DJ on lane
+// 0, then the warp-cooperative reference-exact DFS.  Shared memory per warp:
+// WRX state + snapshots + dependency lags + entry memory.
+__host__ __device__ inline int rep_warp_smem_words(const int *pool) {
+  const int K = pool[R_K];
+  return ((wrx_state_words(K, pool[R_MAXDI]) + 3) & ~3) + (int)wrx_snap_words(K) +
+         (pool[R_NDEP] > 0 ? pool[R_NDEP] : 1) + pool[R_D] + 2;
+}
+
+__global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gpool,
+                                                      const unsigned char *__restrict__ assign,
+                                                      const int *__restrict__ def_in, int n_def,
+                                                      ProbeOut o, int P, long long full_budget,
+                                                      long long stage_budget,
+                                                      long long dj_budget, int cap,
+                                                      long long widx_limit,
+                                                      unsigned long long budget_ns,
+                                                      int *ws_base, long long ws_words) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int per_warp = rep_warp_smem_words(sp);
+  int *mine_s = sp + ((sp[R_WORDS] + 3) & ~3) + wib * ((per_warp + 3) & ~3);
+  const int ndep1 = sp[R_NDEP] > 0 ? sp[R_NDEP] : 1;
+  int *snap = mine_s + ((wrx_state_words(K, sp[R_MAXDI]) + 3) & ~3);  // int2-aligned
+  int *deplag = snap + (int)wrx_snap_words(K);
+  int *init = deplag + ndep1;
+  WWs w = wrx_carve(mine_s, snap, K, sp[R_MAXDI]);
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  int *mine_g = ws_base + gw * ws_words;  // lane-0 DJ workspace
+  DjWs dw = dj_ws_carve(mine_g, K, sp[R_D], sp[R_NPAIR], sp[R_MAXDI]);
+  const bool partial = stage_budget > 0 && (full_budget == 0 || stage_budget < full_budget);
+  const long long rx_budget = partial ? stage_budget : full_budget;
+  unsigned long long s_nodes = 0, s_cap = 0, s_sat = 0, s_dju = 0, s_djn = 0, s_def = 0;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long t = gw; t < n_def; t += nwarps) {
+    const int widx = def_in[t];
+    if (widx > widx_limit) continue;
+    const unsigned char *a = assign + (long long)widx * K;
+    const unsigned long long t_end = budget_ns ? rx_now_ns() + budget_ns : 0ull;
+    int dj = DJ_UNKNOWN;
+    if (dj_budget > 0) {
+      if (lane == 0) {
+        rep_prepare(sp, a, P, deplag, init, dw.lo, dw.hi);
+        const RepView v = rep_view(sp, P, cap, deplag, init);
+        long long dn = 0;
+        dj = dj_decide(v, sp, dw, dj_budget, &dn);
+        s_djn += (unsigned long long)dn;
+      }
+      dj = __shfl_sync(WRX_FULL, dj, 0);
+    }
+    if (dj == DJ_UNSAT) {
+      if (lane == 0) {
+        ++s_dju;
+        o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
+      }
+      continue;
+    }
+    if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
+    __syncwarp();
+    const RepView v = rep_view(sp, P, cap, deplag, init);
+    long long nd = 0;
+    const int st = wrx_decide(v, w, rx_budget, t_end, &nd);
+    if (st == RX_SAT) {
+      int k = 0;
+      if (lane == 0) k = atomicAdd(&o.counters[1], 1);
+      k = __shfl_sync(WRX_FULL, k, 0);
+      if (lane == 0) o.sat_widx[k] = widx;
+      for (int i = lane; i < K; i += 32) o.sat_starts[(long long)k * K + i] = w.s[i];
+      if (lane == 0) {
+        s_nodes += (unsigned long long)nd;
+        ++s_sat;
+      }
+    } else if (lane == 0) {
+      if (st == RX_TIMEOUT && partial) {
+        ++s_def;
+        o.def_out[atomicAdd(&o.counters[2], 1)] = widx;
+      } else {
+        s_nodes += (unsigned long long)nd;
+        if (st == RX_TIMEOUT) ++s_cap;
+        o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    atomicAdd(&o.stats[5], s_def);
+    atomicAdd(&o.stats[2], s_nodes);
+    atomicAdd(&o.stats[3], s_cap);
+    atomicAdd(&o.stats[4], s_sat);
+    atomicAdd(&o.stats[6], s_dju);
+    atomicAdd(&o.stats[7], s_djn);
   }
 }
 
@@ -241,6 +466,13 @@ DecideCtx &decide_ctx() {
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+// TSL_DFS_MODE=thread selects the one-thread-per-probe DFS kernels (kept for
+// cross-validation); the default is the warp-cooperative DFS.
+bool decide_mode_warp() {
+  const char *m = getenv("TSL_DFS_MODE");
+  return !(m && std::string(m) == "thread");
+}
+
 void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, int32_t *status,
                       int64_t *nodes, int64_t *starts, int stride) {
   require_device();
@@ -248,7 +480,8 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
   std::vector<int> pools;
   std::vector<long long> pool_off(count), ws_off(count), budgets(count);
   long long ws_total = 0;
-  int max_n = 0;
+  int max_n = 0, max_state = 0;
+  const bool warp_mode = decide_mode_warp();
   for (int i = 0; i < count; ++i) {
     const tsl_problem &p = probs[i];
     std::vector<int> one = tsl::gen_build(p.n, p.dur, p.devmask, p.mem, p.edges, p.m, p.order,
@@ -256,7 +489,12 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
     pool_off[i] = (long long)pools.size();
     pools.insert(pools.end(), one.begin(), one.end());
     ws_off[i] = ws_total;
-    ws_total += (rx_ws_words(p.n, one[G_MAXDI]) + 3) / 4 * 4;
+    if (warp_mode) {
+      ws_total += (wrx_snap_words(p.n) + 3) / 4 * 4;
+      max_state = std::max(max_state, wrx_state_words(p.n, one[G_MAXDI]));
+    } else {
+      ws_total += (rx_ws_words(p.n, one[G_MAXDI]) + 3) / 4 * 4;
+    }
     budgets[i] = p.node_budget < 0 ? 0 : p.node_budget;
     max_n = std::max(max_n, p.n);
   }
@@ -297,8 +535,17 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
       budget_secs > 0 ? (unsigned long long)(budget_secs * 1e9) : 0ull;
   const int threads = 32;
   COUNT_LAUNCH();
-  k_decide_batch<<<(count + threads - 1) / threads, threads, 0, s>>>(
-      d_pools, d_poff, count, d_bud, budget_ns, d_ws, d_woff, d_st, d_nd, d_starts, stride);
+  if (warp_mode) {
+    const size_t smem = (size_t)max_state * sizeof(int);
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_decide_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+    k_decide_warp<<<count, 32, smem, s>>>(d_pools, d_poff, count, d_bud, budget_ns, d_ws,
+                                          d_woff, d_st, d_nd, d_starts, stride);
+  } else {
+    k_decide_batch<<<(count + threads - 1) / threads, threads, 0, s>>>(
+        d_pools, d_poff, count, d_bud, budget_ns, d_ws, d_woff, d_st, d_nd, d_starts, stride);
+  }
   CK(cudaGetLastError());
   std::vector<int> h_st(count);
   std::vector<long long> h_nd(count);
@@ -342,6 +589,9 @@ struct tsl_engine {
   int cur = 0;
   unsigned char *d_assign = nullptr, *d_gate = nullptr;
   int *d_act[2] = {nullptr, nullptr};
+  int *d_def[2] = {nullptr, nullptr};
+  int dcur = 0;
+  long long n_def = 0, n_sat = 0;
   int *d_sat_widx = nullptr, *d_sat_starts = nullptr;
   int *d_counters = nullptr;
   unsigned long long *d_stats = nullptr;
@@ -380,13 +630,16 @@ struct tsl_engine {
     if (smem_bytes > 48 * 1024) {
       CK(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem_bytes));
+      CK(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem_bytes));
       CK(cudaFuncSetAttribute(k_stage, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem_bytes));
     }
     const int K = pool[R_K];
     const int ndep = pool[R_NDEP];
-    ws_words = rx_ws_words(K, pool[R_MAXDI]) + std::max(ndep, 1) + pool[R_D];
-    ws_words = (ws_words + 31) / 32 * 32;
+    (void)K;
+    (void)ndep;
+    ws_words = rep_ws_words(pool.data());
     ws_threads = num_sms * 4 * 128;
     CK(cudaMalloc(&d_ws, (size_t)ws_threads * ws_words * sizeof(int)));
     gpu_ready = true;
@@ -414,13 +667,16 @@ struct tsl_engine {
   void ensure_window(long long w) {
     if (w <= W_cap) return;
     for (void *p : {(void *)d_assign, (void *)d_gate, (void *)d_act[0], (void *)d_act[1],
-                    (void *)d_sat_widx, (void *)d_sat_starts})
+                    (void *)d_sat_widx, (void *)d_sat_starts, (void *)d_def[0],
+                    (void *)d_def[1]})
       if (p) CK(cudaFree(p));
     const int K = pool[R_K];
     CK(cudaMalloc(&d_assign, (size_t)w * K));
     CK(cudaMalloc(&d_gate, (size_t)w));
     CK(cudaMalloc(&d_act[0], (size_t)w * sizeof(int)));
     CK(cudaMalloc(&d_act[1], (size_t)w * sizeof(int)));
+    CK(cudaMalloc(&d_def[0], (size_t)w * sizeof(int)));
+    CK(cudaMalloc(&d_def[1], (size_t)w * sizeof(int)));
     CK(cudaMalloc(&d_sat_widx, (size_t)w * sizeof(int)));
     CK(cudaMalloc(&d_sat_starts, (size_t)w * K * sizeof(int)));
     W_cap = w;
@@ -430,7 +686,8 @@ struct tsl_engine {
     if (!gpu_ready) return;
     for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
-                    (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather})
+                    (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather,
+                    (void *)d_def[0], (void *)d_def[1]})
       if (p) cudaFree(p);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -601,10 +858,47 @@ int tsl_engine_stage(tsl_engine *e, int n_r, uint64_t r0, uint64_t r1, int64_t c
   API_END
 }
 
-int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap,
-                     int64_t widx_limit, double budget_secs, int64_t max_sat,
+static void fill_stats(const unsigned long long *st, tsl_level_stats *stats) {
+  if (!stats) return;
+  stats->probes = (int64_t)st[0];
+  stats->root_refuted = (int64_t)st[1];
+  stats->nodes = (int64_t)st[2];
+  stats->capped = (int64_t)st[3];
+  stats->sat = (int64_t)st[4];
+  stats->deferred = (int64_t)st[5];
+  stats->dj_refuted = (int64_t)st[6];
+  stats->dj_nodes = (int64_t)st[7];
+}
+
+// Fetch the SAT count of the level, sort the (window index, row) list on the
+// host and return the first max_sat rows.
+static int finish_level(tsl_engine *e, int n_sat, int64_t max_sat, int64_t *out_nsat,
+                        int64_t *sat_widx, int32_t *sat_starts) {
+  std::vector<int> widx(n_sat);
+  if (n_sat > 0) {
+    d2h(widx.data(), e->d_sat_widx, n_sat * sizeof(int), e->stream);
+    CK(cudaStreamSynchronize(e->stream));
+  }
+  std::vector<int> perm(n_sat);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::sort(perm.begin(), perm.end(), [&](int x, int y) { return widx[x] < widx[y]; });
+  e->sat_widx_sorted.resize(n_sat);
+  e->sat_pos_sorted.resize(n_sat);
+  for (int r = 0; r < n_sat; ++r) {
+    e->sat_widx_sorted[r] = widx[perm[r]];
+    e->sat_pos_sorted[r] = perm[r];
+  }
+  e->n_sat = n_sat;
+  *out_nsat = n_sat;
+  const long long keep = std::min<long long>(n_sat, max_sat < 0 ? 0 : max_sat);
+  if (keep > 0) return tsl_engine_sat_rows(e, 0, keep, sat_widx, sat_starts);
+  return TSL_OK;
+}
+
+int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t small_budget,
+                     int64_t cap, int64_t widx_limit, double budget_secs, int64_t max_sat,
                      int64_t *out_nsat, int64_t *sat_widx, int32_t *sat_starts,
-                     int64_t *out_active, tsl_level_stats *stats) {
+                     int64_t *out_active, int64_t *out_deferred, tsl_level_stats *stats) {
   API_BEGIN
   if (!e->gpu_ready) throw tsl::Error(TSL_EINVAL, "tsl_engine_probe before tsl_engine_stage");
   CK(cudaSetDevice(e->device));
@@ -620,14 +914,21 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap
   blocks = std::max(1LL, std::min<long long>(blocks, (long long)e->ws_threads / threads));
   const unsigned long long budget_ns =
       budget_secs > 0 ? (unsigned long long)(budget_secs * 1e9) : 0ull;
+  ProbeOut o;
+  o.act_out = e->d_act[1 - e->cur];
+  e->dcur = 0;
+  o.def_out = e->d_def[0];
+  o.sat_widx = e->d_sat_widx;
+  o.sat_starts = e->d_sat_starts;
+  o.counters = e->d_counters;
+  o.stats = e->d_stats;
   CK(cudaEventRecord(e->ev0, e->stream));
   if (n_in > 0) {
     COUNT_LAUNCH();
     k_probe<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
-        e->d_pool, e->d_assign, e->d_act[e->cur], (int)n_in, e->d_act[1 - e->cur],
-        e->d_counters, e->d_sat_widx, e->d_sat_starts, period,
-        node_budget < 0 ? 0 : node_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words,
-        e->d_stats);
+        e->d_pool, e->d_assign, e->d_act[e->cur], (int)n_in, o, period,
+        node_budget < 0 ? 0 : node_budget, small_budget <= 0 ? 0 : small_budget, icap,
+        widx_limit, budget_ns, e->d_ws, e->ws_words);
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(e->ev1, e->stream));
@@ -637,38 +938,80 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t cap
   d2h(st, e->d_stats, 8 * sizeof(unsigned long long), e->stream);
   CK(cudaStreamSynchronize(e->stream));
   CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
-  const int n_out = counters[0], n_sat = counters[1];
-  std::vector<int> widx(n_sat);
-  if (n_sat > 0) {
-    d2h(widx.data(), e->d_sat_widx, n_sat * sizeof(int), e->stream);
-    CK(cudaStreamSynchronize(e->stream));
-  }
-  std::vector<int> perm(n_sat);
-  std::iota(perm.begin(), perm.end(), 0);
-  std::sort(perm.begin(), perm.end(), [&](int x, int y) { return widx[x] < widx[y]; });
-  e->sat_widx_sorted.resize(n_sat);
-  e->sat_pos_sorted.resize(n_sat);
-  for (int r = 0; r < n_sat; ++r) {
-    e->sat_widx_sorted[r] = widx[perm[r]];
-    e->sat_pos_sorted[r] = perm[r];
-  }
-  const long long keep = std::min<long long>(n_sat, max_sat < 0 ? 0 : max_sat);
-  if (keep > 0) {
-    const int rc = tsl_engine_sat_rows(e, 0, keep, sat_widx, sat_starts);
-    if (rc < 0) return rc;
-  }
-  *out_nsat = n_sat;
   e->cur = 1 - e->cur;
-  e->n_act = n_out;
-  *out_active = n_out;
-  if (stats) {
-    stats->probes = (int64_t)st[0];
-    stats->root_refuted = (int64_t)st[1];
-    stats->nodes = (int64_t)st[2];
-    stats->capped = (int64_t)st[3];
-    stats->sat = (int64_t)st[4];
+  e->n_act = counters[0];
+  e->n_def = counters[2];
+  *out_active = counters[0];
+  *out_deferred = counters[2];
+  fill_stats(st, stats);
+  return finish_level(e, counters[1], max_sat, out_nsat, sat_widx, sat_starts);
+  API_END
+}
+
+int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t stage_budget,
+                       int64_t dj_budget, int64_t cap, int64_t widx_limit, double budget_secs,
+                       int64_t max_sat, int64_t *out_nsat, int64_t *sat_widx,
+                       int32_t *sat_starts, int64_t *out_active, int64_t *out_deferred,
+                       tsl_level_stats *stats) {
+  API_BEGIN
+  if (!e->gpu_ready) throw tsl::Error(TSL_EINVAL, "tsl_engine_resolve before tsl_engine_stage");
+  CK(cudaSetDevice(e->device));
+  const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
+  const long long n_def = e->n_def;
+  // continue appending to the level's SAT list and to the active list
+  int counters[4] = {(int)e->n_act, (int)e->n_sat, 0, 0};
+  h2d(e->d_counters, counters, 4 * sizeof(int), e->stream);
+  CK(cudaMemsetAsync(e->d_stats, 0, 8 * sizeof(unsigned long long), e->stream));
+  const int threads = 128;
+  long long blocks = (n_def + threads - 1) / threads;
+  blocks = std::max(1LL, std::min<long long>(blocks, (long long)e->ws_threads / threads));
+  const unsigned long long budget_ns =
+      budget_secs > 0 ? (unsigned long long)(budget_secs * 1e9) : 0ull;
+  ProbeOut o;
+  o.act_out = e->d_act[e->cur];
+  o.def_out = e->d_def[1 - e->dcur];
+  o.sat_widx = e->d_sat_widx;
+  o.sat_starts = e->d_sat_starts;
+  o.counters = e->d_counters;
+  o.stats = e->d_stats;
+  CK(cudaEventRecord(e->ev0, e->stream));
+  if (n_def > 0 && decide_mode_warp()) {
+    const int wpb = 4;
+    long long wblocks = (n_def + wpb - 1) / wpb;
+    wblocks = std::max(1LL, std::min<long long>(wblocks, (long long)e->ws_threads / (32 * wpb)));
+    const size_t smem = (size_t)(((e->pool.size() + 3) & ~(size_t)3) +
+                                 wpb * ((rep_warp_smem_words(e->pool.data()) + 3) & ~3)) *
+                        sizeof(int);
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_resolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+    COUNT_LAUNCH();
+    k_resolve_warp<<<(int)wblocks, 32 * wpb, smem, e->stream>>>(
+        e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, o, period,
+        node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? 0 : stage_budget,
+        dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words);
+    CK(cudaGetLastError());
+  } else if (n_def > 0) {
+    COUNT_LAUNCH();
+    k_resolve<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
+        e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, o, period,
+        node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? 0 : stage_budget,
+        dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words);
+    CK(cudaGetLastError());
   }
-  return TSL_OK;
+  CK(cudaEventRecord(e->ev1, e->stream));
+  unsigned long long st[8] = {0};
+  d2h(counters, e->d_counters, 4 * sizeof(int), e->stream);
+  d2h(st, e->d_stats, 8 * sizeof(unsigned long long), e->stream);
+  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
+  e->n_act = counters[0];
+  e->n_def = counters[2];
+  e->dcur = 1 - e->dcur;
+  *out_active = counters[0];
+  *out_deferred = counters[2];
+  fill_stats(st, stats);
+  return finish_level(e, counters[1], max_sat, out_nsat, sat_widx, sat_starts);
   API_END
 }
 

@@ -24,6 +24,7 @@ lower-index completion-feasible SAT y at a period <= P bounds it
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -38,6 +39,13 @@ WINDOW_FIRST = 2048
 WINDOW_GROWTH = 4
 WINDOW_MAX = 1 << 21
 SAT_CHUNK = 256
+SMALL_BUDGET = 64     # first-pass RX-DFS nodes per probe (thread per probe) before deferral
+DJ_BUDGET = 200_000   # disjunctive-refutation nodes per deferred probe
+# escalation of deferred probes: (DJ budget, RX-DFS stage budget; 0 = the
+# reference cap).  The retirement limit is re-applied between stages, so a
+# probe above the lowest completion-feasible SAT never runs the full cap.
+RESOLVE_STAGES = ((DJ_BUDGET, 32_768), (0, 0))
+TRACE = os.environ.get("TESSEL_TRACE", "0") == "1"
 
 
 @dataclass
@@ -50,17 +58,21 @@ class EngineCounters:
     nodes: int = 0
     capped: int = 0
     sat: int = 0
+    deferred: int = 0
+    dj_refuted: int = 0
+    dj_nodes: int = 0
     kernel_ms: float = 0.0
     launches: int = 0
+    trace: list = field(default_factory=list)
 
-    def add_level(self, st: dict, ms: float):
-        self.levels += 1
+    def add(self, st: dict, ms: float, level: bool, tag=None):
+        if TRACE and tag is not None:
+            self.trace.append((*tag, round(ms, 3), {k: v for k, v in st.items() if v}))
+        self.levels += level
         self.launches += 1
-        self.probes += st["probes"]
-        self.root_refuted += st["root_refuted"]
-        self.nodes += st["nodes"]
-        self.capped += st["capped"]
-        self.sat += st["sat"]
+        for k in ("probes", "root_refuted", "nodes", "capped", "sat", "deferred", "dj_refuted",
+                  "dj_nodes"):
+            setattr(self, k, getattr(self, k) + st[k])
         self.kernel_ms += ms
 
 
@@ -87,6 +99,26 @@ class BatchedRepetendSearch:
         self.lb = lower_bound(p)
         self.total = sum(dur)
         self.counters = EngineCounters()
+        self.small_budget = SMALL_BUDGET
+        self.resolve_stages = RESOLVE_STAGES
+
+    def _scan_sats(self, res, n_r, r0, period, n_sat, widx, rows, limit, feasible):
+        """Walk the level's SAT rows in window order up to the first
+        completion-feasible one; it retires every higher index."""
+        i, start = 0, 0
+        while i < n_sat:
+            if i >= start + len(widx):
+                start = i
+                widx, rows = self.eng.sat_rows(i, min(SAT_CHUNK, n_sat - i))
+            j = i - start
+            w = int(widx[j])
+            if w > limit:
+                break
+            res.first_sat[w] = (period, rows[j].copy())
+            if feasible(n_r, r0 + w, period, rows[j]):
+                return w - 1
+            i += 1
+        return limit
 
     def count(self, n_r: int) -> int:
         return self.eng.count(n_r)
@@ -106,7 +138,7 @@ class BatchedRepetendSearch:
         res = WindowResult(n_r, r0, r1 - r0)
         n_act, gate = self.eng.stage(n_r, r0, r1, cap, want_gate=cap is not None)
         self.counters.windows += 1
-        self.counters.launches += 1
+        self.counters.launches += 1  # k_stage
         self.counters.kernel_ms += self.eng.last_kernel_ms()
         res.gate = gate
         limit = res.count - 1
@@ -122,24 +154,24 @@ class BatchedRepetendSearch:
                     return res
                 budget_secs = left
             node_cap = 0 if period == self.lb else PROBE_NODES
-            n_sat, widx, rows, n_act, st = self.eng.probe(period, node_cap, cap, limit,
-                                                          budget_secs, SAT_CHUNK)
-            self.counters.add_level(st, self.eng.last_kernel_ms())
+            n_sat, widx, rows, n_act, n_def, st = self.eng.probe(
+                period, node_cap, self.small_budget, cap, limit, budget_secs, SAT_CHUNK)
+            self.counters.add(st, self.eng.last_kernel_ms(), True, (n_r, r0, period, "probe"))
             if deadline and st["capped"] and time.monotonic() > deadline:
                 res.timed_out = True
                 return res
-            i, start = 0, 0
-            while i < n_sat:
-                if i >= start + len(widx):
-                    start = i
-                    widx, rows = self.eng.sat_rows(i, min(SAT_CHUNK, n_sat - i))
-                j = i - start
-                w = int(widx[j])
-                if w > limit:
+            limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit, feasible)
+            for dj_budget, stage_budget in self.resolve_stages:
+                if not n_def:
                     break
-                res.first_sat[w] = (period, rows[j].copy())
-                if feasible(n_r, r0 + w, period, rows[j]):
-                    limit = w - 1
-                    break
-                i += 1
+                n_sat, widx, rows, n_act, n_def, st = self.eng.resolve(
+                    period, node_cap, stage_budget, dj_budget, cap, limit, budget_secs,
+                    SAT_CHUNK)
+                self.counters.add(st, self.eng.last_kernel_ms(), False,
+                                  (n_r, r0, period, f"resolve{stage_budget}"))
+                if deadline and st["capped"] and time.monotonic() > deadline:
+                    res.timed_out = True
+                    return res
+                limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit,
+                                        feasible)
         return res

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../paper_2311_15269_b200/csrc/host_build.hpp"
+#include "../../paper_2311_15269_b200/csrc/dj_solve.cuh"
 
 template <class T>
 static std::vector<T> rd(int k) {
@@ -56,7 +57,10 @@ int main() {
       long long nodes = 0;
       int st = rx_decide(g, w, budget, 0ull, &nodes);
       emit(st, nodes, w.s, n);
-    } else if (tag == "R") {
+    } else if (tag == "R" || tag == "J") {
+      // "J": same input as "R"; runs the disjunctive refutation (dj_decide)
+      // and prints "verdict dj_nodes"
+      const bool dj = tag == "J";
       tsl::Placement pl;
       int ndep;
       std::cin >> pl.K >> pl.D >> ndep;
@@ -71,6 +75,8 @@ int main() {
       std::vector<int> ws(rx_ws_words(K, pool[R_MAXDI]) + 8), coef(std::max(ndep, 1)),
           init(pl.D);
       RxWs w = rx_ws_carve(ws.data(), K, pool[R_MAXDI]);
+      std::vector<int> dws(dj_ws_words(K, pl.D, pool[R_NPAIR], pool[R_MAXDI]) + 8);
+      DjWs dw = dj_ws_carve(dws.data(), K, pl.D, pool[R_NPAIR], pool[R_MAXDI]);
       int nq;
       std::cin >> nq;
       for (int q = 0; q < nq; ++q) {
@@ -79,14 +85,16 @@ int main() {
         std::cin >> P >> cap >> budget;
         auto a = rd<int>(K);
         const int *ap = a.data();
-        rep_prepare(pool.data(), ap, P, coef.data(), init.data(), w.lo, w.hi);
-        RepView v;
-        v.pool = pool.data();
-        v.coef = coef.data();
-        v.init = init.data();
-        v.P = P;
-        v.cap_ = cap < 0 ? -1 : (int)cap;
+        const RepView v =
+            rep_view(pool.data(), P, cap < 0 ? -1 : (int)cap, coef.data(), init.data());
         long long nodes = 0;
+        if (dj) {
+          rep_prepare(pool.data(), ap, P, coef.data(), init.data(), dw.lo, dw.hi);
+          const int st = dj_decide(v, pool.data(), dw, budget, &nodes);
+          std::printf("%d %lld\n", st, nodes);
+          continue;
+        }
+        rep_prepare(pool.data(), ap, P, coef.data(), init.data(), w.lo, w.hi);
         int st = rx_decide(v, w, budget, 0ull, &nodes);
         emit(st, nodes, w.s, K);
       }

@@ -31,6 +31,17 @@ def test_decide_batch_matches_reference_probes(gpu, name):
         assert (st, s, nodes) == (p["status"], p["starts"], p["nodes"]), (name, p["kind"])
 
 
+@pytest.mark.parametrize("name", ["C1", "C2_3", "nn4_k3", "C5_2"])
+def test_decide_thread_kernel_matches_reference_probes(gpu, name, monkeypatch):
+    """The one-thread-per-problem DFS kernel (TSL_DFS_MODE=thread) is kept as
+    a cross-check of the default warp-cooperative kernel."""
+    monkeypatch.setenv("TSL_DFS_MODE", "thread")
+    probes = [p for p in load_probes(name) if p["kind"] != "capped"]
+    got = gpu.decide_batch([_problem(p) for p in probes])
+    for p, r in zip(probes, got):
+        assert r == (p["status"], p["starts"], p["nodes"]), (name, p["kind"])
+
+
 def test_decide_single_and_core_seam(gpu):
     from paper_2311_15269_b200 import _core
 

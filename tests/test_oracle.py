@@ -175,3 +175,41 @@ def test_reference_crosscheck_when_available():
         budget = rng.choice((0, 0, 5, 50))
         args = (n, dur, mask, mem, edges, order, lo, hi, ndev, init, cap, budget, 0.0)
         assert oracle.decide(*args) == RC.decide(*args)
+
+
+def test_disjunctive_filter_never_refutes_a_feasible_probe(rx_host):
+    """DJ (csrc/dj_solve.cuh) is used only to prove repetend probes
+    infeasible.  On the probes the reference node-caps (plus DFS-heavy ones)
+    it must never answer UNSAT when the probe is feasible, and it must agree
+    with the oracle's exact verdict whenever it decides."""
+    import json
+    from collections import defaultdict
+
+    from paper_2311_15269_b200.workloads import WORKLOADS
+
+    path = GOLDEN / "dj_probes.json"
+    if not path.exists():
+        pytest.skip("dj_probes.json not generated")
+    rows = json.loads(path.read_text())
+    by_wl = defaultdict(list)
+    for r in rows:
+        by_wl[r["workload"]].append(r)
+    decided = refuted_capped = capped = 0
+    for wl, rs in by_wl.items():
+        p = WORKLOADS[wl].placement()
+        qs = [(r["a"], r["P"], -1 if r["cap"] is None else r["cap"], 200_000) for r in rs]
+        out = subprocess.run([str(rx_host)], input=_rep_block(p, qs).replace("R ", "J ", 1) + "\n",
+                             capture_output=True, text=True, check=True).stdout.split("\n")
+        for r, line in zip(rs, out):
+            verdict, _ = map(int, line.split())
+            if r["truth"] == 1:
+                assert verdict != 0, (wl, r["a"], r["P"])
+            if verdict != 2 and r["truth"] != -1:
+                decided += 1
+                assert verdict == r["truth"], (wl, r["a"], r["P"])
+            if r["ref_status"] == 2:
+                capped += 1
+                refuted_capped += verdict == 0
+    assert decided > 0
+    # the filter is only useful if it settles most reference-capped probes
+    assert capped == 0 or refuted_capped / capped > 0.5
