@@ -178,26 +178,33 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def _roofline(kernel_ms_probe, probes, clocks):
-    """Issue roofline of k_probe: warp instructions per probe from the
-    committed ncu capture × live probes ÷ live kernel time."""
-    prof = ROOT / "profiles" / "inst_counts.json"
+def _roofline(kernel_ms: dict, steps: int, workload: str):
+    """Issue roofline of the dominant kernel (largest live CUDA-event time).
+
+    achieved = warp instructions the kernel issues per step (deterministic
+    for a given workload; counted once with ncu smsp__inst_executed.sum over a
+    full search, committed in profiles/inst_counts.json) ÷ the kernel's live
+    per-step time measured here with CUDA events on the engine stream.
+    peak = 148 SMs x 4 warp-schedulers x 1 instr/clk x sm_max_mhz."""
     peaks = {}
     mp = ROOT / "MEASURED_PEAKS.json"
     if mp.exists():
         peaks = json.loads(mp.read_text())
     mhz = peaks.get("sm_max_mhz", 1965.0)
-    peak = 148 * 4 * mhz * 1e6  # warp-instructions / s (4 schedulers per SM)
-    out = {"bound": "issue", "unit": "warp-inst/s", "peak": peak,
+    peak = 148 * 4 * mhz * 1e6
+    kern = max(kernel_ms, key=kernel_ms.get)
+    out = {"bound": "issue", "unit": "warp-inst/s", "peak": peak, "kernel": kern,
+           "kernel_ms_per_step": {k: v / steps for k, v in kernel_ms.items()},
            "peak_basis": f"148 SMs x 4 issue/clk x {mhz} MHz (MEASURED_PEAKS sm_max_mhz)",
            "achieved": None, "frac": None, "traffic": None}
-    if prof.exists() and kernel_ms_probe > 0:
+    prof = ROOT / "profiles" / "inst_counts.json"
+    if prof.exists():
         d = json.loads(prof.read_text())
-        ipp = d.get("k_probe", {}).get("warp_inst_per_probe")
-        if ipp:
-            ach = ipp * probes / (kernel_ms_probe / 1e3)
-            out.update(achieved=ach, frac=ach / peak,
-                       traffic=d.get("k_probe", {}).get("dram_bytes_per_launch"),
+        k = d.get("per_step", {}).get(kern) if d.get("workload") == workload else None
+        if k and kernel_ms[kern] > 0:
+            ach = k["warp_inst"] / (kernel_ms[kern] / steps / 1e3)
+            out.update(achieved=ach, frac=ach / peak, traffic=k.get("dram_bytes"),
+                       traffic_basis="ncu dram__bytes_read+write per step for this kernel",
                        basis=d.get("basis"))
     return out
 
@@ -231,6 +238,7 @@ def run_b200_arm(args):
     parity = _matches(res, golden) if args.warmup else None
 
     kernel_ms = 0.0
+    per_kernel = {"k_probe": 0.0, "k_resolve_warp": 0.0, "k_stage": 0.0}
     cands = 0
     walls = []
     stats = {"probes": 0, "nodes": 0, "capped": 0, "root_refuted": 0, "levels": 0}
@@ -242,6 +250,7 @@ def run_b200_arm(args):
         for _ in range(args.steps):
             _flush_l2(torch, dev)               # L2 flushed between timed steps
             e0 = eng.counters.kernel_ms
+            k0 = (eng.counters.probe_ms, eng.counters.resolve_ms, eng.counters.stage_ms)
             n0 = {k: getattr(eng.counters, k) for k in stats}
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
@@ -249,6 +258,9 @@ def run_b200_arm(args):
             torch.cuda.synchronize(dev)
             walls.append(time.perf_counter() - t0)
             kernel_ms += eng.counters.kernel_ms - e0
+            per_kernel["k_probe"] += eng.counters.probe_ms - k0[0]
+            per_kernel["k_resolve_warp"] += eng.counters.resolve_ms - k0[1]
+            per_kernel["k_stage"] += eng.counters.stage_ms - k0[2]
             cands += len(res.report.candidates)
             for k in stats:
                 stats[k] += getattr(eng.counters, k) - n0[k]
@@ -288,7 +300,7 @@ def run_b200_arm(args):
         "gpu_launches": launches,
         "work_per_step": {k: v // args.steps for k, v in stats.items()},
         "clocks": clocks,
-        "roofline": _roofline(kernel_ms, stats["probes"], clocks),
+        "roofline": _roofline(per_kernel, args.steps, args.workload),
     }
     if not args.no_cpu_baseline:
         kind, n, cwall, _ = reference_search(p, w.mem_capacity, w.max_nr, args.ref_sample_secs, 1)

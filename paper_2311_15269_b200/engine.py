@@ -62,10 +62,17 @@ class EngineCounters:
     dj_refuted: int = 0
     dj_nodes: int = 0
     kernel_ms: float = 0.0
+    probe_ms: float = 0.0     # k_probe (first pass)
+    resolve_ms: float = 0.0   # k_resolve_warp (DJ + warp RX-DFS stages)
+    stage_ms: float = 0.0     # k_stage (unrank + gate)
     launches: int = 0
     trace: list = field(default_factory=list)
 
     def add(self, st: dict, ms: float, level: bool, tag=None):
+        if level:
+            self.probe_ms += ms
+        else:
+            self.resolve_ms += ms
         if TRACE and tag is not None:
             self.trace.append((*tag, round(ms, 3), {k: v for k, v in st.items() if v}))
         self.levels += level
@@ -140,6 +147,7 @@ class BatchedRepetendSearch:
         self.counters.windows += 1
         self.counters.launches += 1  # k_stage
         self.counters.kernel_ms += self.eng.last_kernel_ms()
+        self.counters.stage_ms += self.eng.last_kernel_ms()
         res.gate = gate
         limit = res.count - 1
         top = min(self.total, bound - 1)
