@@ -18,6 +18,7 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 from .engine import WINDOW_FIRST, WINDOW_GROWTH, WINDOW_MAX, BatchedRepetendSearch
+from .parallel import LevelSync, split_range
 from .placement import BlockInstance, PlacementSpec
 from .repetend import (Repetend, RepetendOutcome, entry_memory, lower_bound, make_repetend,
                        steady_memory_ok)
@@ -305,8 +306,8 @@ class _Feasibility:
 
 def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optional[int] = None,
            lazy: bool = True, budget: Optional[float] = None, jobs: int = 1,
-           device: Optional[int] = None, engine: Optional[BatchedRepetendSearch] = None
-           ) -> SearchResult:
+           device: Optional[int] = None, engine: Optional[BatchedRepetendSearch] = None,
+           comm=None) -> SearchResult:
     """Two-phase schedule search: repetend construction, then completion
     (completion.py:284-396).  ``jobs`` is accepted for API compatibility;
     candidate parallelism comes from the GPU windows instead of a process
@@ -349,16 +350,28 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
                 done = True
                 break
             r1 = min(count, r0 + width)
-            win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
+            if comm is not None:  # rank-prefix shard of the window (parallel.py)
+                a0, b0 = split_range(r0, r1, comm.rank, comm.size)
+                win = eng.evaluate_window(n_r, a0, b0, cap, optimal, feasible, 0.0,
+                                          LevelSync(comm, a0 - r0))
+            else:
+                a0 = r0
+                win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
             if win.timed_out:
                 report.timed_out = True
                 done = True
                 break
+            first_sat = {a0 - r0 + w: v for w, v in win.first_sat.items()}
+            if comm is not None:
+                merged: dict = {}
+                for part in comm.allgather(first_sat):
+                    merged.update(part)
+                first_sat = merged
             # ordered replay (completion.py:351-382)
             special: dict = {}
-            used = win.count
-            for widx in sorted(win.first_sat):
-                period, starts = win.first_sat[widx]
+            used = r1 - r0
+            for widx in sorted(first_sat):
+                period, starts = first_sat[widx]
                 if period >= optimal:
                     continue  # first SAT beyond this candidate's bound: "bound"
                 a = eng.unrank(n_r, r0 + widx)
@@ -378,7 +391,10 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
                     break
             infeasible = 0
             if win.gate is not None:
-                infeasible = int(used - win.gate[:used].sum())
+                mine = max(0, min(win.count, r0 + used - a0))
+                infeasible = int(mine - win.gate[:mine].sum())
+                if comm is not None:
+                    infeasible = comm.allreduce_sum([infeasible])[0]
             log.add_segment(n_r, r0, used, special, infeasible)
             r0 = r1
             width = min(width * WINDOW_GROWTH, WINDOW_MAX)

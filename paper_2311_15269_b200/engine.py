@@ -91,18 +91,23 @@ class WindowResult:
     first_sat: dict = field(default_factory=dict)  # widx -> (period, starts)
     gate: Optional[np.ndarray] = None               # 1 = passes the memory gate
     timed_out: bool = False
+    first_feasible: Optional[int] = None            # lowest completion-feasible SAT widx
 
 
 class BatchedRepetendSearch:
     """One placement resident on one GPU."""
 
-    def __init__(self, p: PlacementSpec, device: int = 0):
+    def __init__(self, p: PlacementSpec, device: int = 0, native=None):
+        """``native`` substitutes the low-level engine (tests drive the level
+        logic on CPU with an oracle-backed stand-in); default: the sm_100a
+        library."""
         self.p = p
         k = p.num_stages
         dur = [p.block(s).time_cost for s in range(k)]
         mem = [p.block(s).mem_delta for s in range(k)]
         masks = [sum(1 << d for d in p.block(s).devices) for s in range(k)]
-        self.eng = _native.Engine(dur, mem, masks, sorted(p.deps), p.num_devices, device)
+        self.eng = native if native is not None else _native.Engine(
+            dur, mem, masks, sorted(p.deps), p.num_devices, device)
         self.lb = lower_bound(p)
         self.total = sum(dur)
         self.counters = EngineCounters()
@@ -123,6 +128,7 @@ class BatchedRepetendSearch:
                 break
             res.first_sat[w] = (period, rows[j].copy())
             if feasible(n_r, r0 + w, period, rows[j]):
+                res.first_feasible = w
                 return w - 1
             i += 1
         return limit
@@ -138,10 +144,13 @@ class BatchedRepetendSearch:
 
     def evaluate_window(self, n_r: int, r0: int, r1: int, cap: Optional[int], bound: int,
                         feasible: Callable[[int, int, int, np.ndarray], bool],
-                        deadline: float = 0.0) -> WindowResult:
+                        deadline: float = 0.0, sync=None) -> WindowResult:
         """Level-synchronous period scan of ranks [r0, r1) at n_r under the
         sequential bound ``bound`` in force at the window start.
-        ``feasible(n_r, rank, period, starts)`` is the completion check."""
+        ``feasible(n_r, rank, period, starts)`` is the completion check.
+        ``sync(first_feasible, limit, n_active) -> (limit, any_active)``
+        exchanges the retirement bound with the other shards of the window
+        (parallel.LevelSync); None = single shard."""
         res = WindowResult(n_r, r0, r1 - r0)
         n_act, gate = self.eng.stage(n_r, r0, r1, cap, want_gate=cap is not None)
         self.counters.windows += 1
@@ -151,8 +160,11 @@ class BatchedRepetendSearch:
         res.gate = gate
         limit = res.count - 1
         top = min(self.total, bound - 1)
+        active = n_act > 0
+        if sync is not None:
+            limit, active = sync(None, limit, n_act)
         for period in range(self.lb, top + 1):
-            if n_act == 0:
+            if not active:
                 break
             budget_secs = 0.0
             if deadline:
@@ -182,4 +194,7 @@ class BatchedRepetendSearch:
                     return res
                 limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit,
                                         feasible)
+            active = n_act > 0
+            if sync is not None:
+                limit, active = sync(res.first_feasible, limit, n_act)
         return res

@@ -1,0 +1,123 @@
+"""TEST-ONLY stand-in for the native engine (paper_2311_15269_b200._native.Engine)
+built on the oracle, so the host-side search logic — level-synchronous scan,
+deferral stages, retirement limits, ordered replay and the multi-rank
+protocol — can be exercised on a machine without a GPU.  Same interface and
+result contract as the sm_100a engine; the disjunctive filter is skipped (it
+only changes how fast "not SAT" is reached, never the outcome)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+from oracle import search_port as SP
+
+STATS = ("probes", "root_refuted", "nodes", "capped", "sat", "deferred", "dj_refuted", "dj_nodes")
+
+
+class OracleEngine:
+    def __init__(self, p):
+        self.p = p
+        self.K = p.num_stages
+        self.model = SP.ProbeModel(p)
+        self._lists = {}
+        self.cands, self.active, self.deferred, self.sats = [], [], [], []
+
+    def _list(self, n_r):
+        if n_r not in self._lists:
+            self._lists[n_r] = list(SP.iter_assignments(self.p, n_r))
+        return self._lists[n_r]
+
+    def close(self):
+        pass
+
+    def last_kernel_ms(self):
+        return 0.0
+
+    def count(self, n_r):
+        return len(self._list(n_r))
+
+    def unrank(self, n_r, rank):
+        return tuple(self._list(n_r)[rank])
+
+    def stage(self, n_r, r0, r1, cap, want_gate=False):
+        self.cands = self._list(n_r)[r0:r1]
+        gate = [cap is None or all(e <= cap for e in SP.entry_memory(self.p, a))
+                for a in self.cands]
+        self.active = [w for w, g in enumerate(gate) if g]
+        self.deferred, self.sats = [], []
+        return len(self.active), (np.array(gate, dtype=np.uint8) if want_gate else None)
+
+    def _probe(self, w, period, cap, budget):
+        a = self.cands[w]
+        return self.model.probe(a, period, cap, SP.entry_memory(self.p, a), budget)
+
+    def _rows(self, max_sat):
+        self.sats.sort(key=lambda r: r[0])
+        k = min(len(self.sats), max_sat)
+        widx = np.array([w for w, _ in self.sats[:k]], dtype=np.int64)
+        rows = np.array([s for _, s in self.sats[:k]], dtype=np.int32).reshape(k, self.K)
+        return len(self.sats), widx, rows
+
+    def probe(self, period, node_budget, small_budget, cap, widx_limit, budget_secs=0.0,
+              max_sat=64):
+        first = small_budget if (node_budget == 0 or small_budget < node_budget) else node_budget
+        st = dict.fromkeys(STATS, 0)
+        act, dfr, self.sats = [], [], []
+        for w in self.active:
+            if w > widx_limit:
+                continue
+            s, starts, nodes = self._probe(w, period, cap, first)
+            st["probes"] += 1
+            if s == oracle.SAT:
+                self.sats.append((w, starts))
+                st["sat"] += 1
+            elif s == oracle.TIMEOUT and first != node_budget:
+                dfr.append(w)
+                st["deferred"] += 1
+            else:
+                act.append(w)
+                st["capped"] += s == oracle.TIMEOUT
+                st["root_refuted"] += s == oracle.UNSAT and nodes == 0
+            st["nodes"] += nodes
+        self.active, self.deferred = act, dfr
+        n, widx, rows = self._rows(max_sat)
+        return n, widx, rows, len(act), len(dfr), st
+
+    def resolve(self, period, node_budget, stage_budget, dj_budget, cap, widx_limit,
+                budget_secs=0.0, max_sat=64):
+        partial = stage_budget > 0 and (node_budget == 0 or stage_budget < node_budget)
+        budget = stage_budget if partial else node_budget
+        st = dict.fromkeys(STATS, 0)
+        redo = []
+        for w in self.deferred:
+            if w > widx_limit:
+                continue
+            s, starts, nodes = self._probe(w, period, cap, budget)
+            if s == oracle.SAT:
+                self.sats.append((w, starts))
+                st["sat"] += 1
+            elif s == oracle.TIMEOUT and partial:
+                redo.append(w)
+                st["deferred"] += 1
+            else:
+                self.active.append(w)
+                st["capped"] += s == oracle.TIMEOUT
+            st["nodes"] += nodes
+        self.deferred = redo
+        n, widx, rows = self._rows(max_sat)
+        return n, widx, rows, len(self.active), len(redo), st
+
+    def sat_rows(self, first, count):
+        self.sats.sort(key=lambda r: r[0])
+        part = self.sats[first:first + count]
+        widx = np.array([w for w, _ in part], dtype=np.int64)
+        rows = np.array([s for _, s in part], dtype=np.int32).reshape(len(part), self.K)
+        return widx, rows
+
+
+def oracle_decide(n, dur, devmask, mem, edges, order, lo, hi, ndev, init_mem, cap,
+                  node_budget=0, deadline=0.0):
+    """Stand-in for paper_2311_15269_b200._core.decide in CPU tests."""
+    return oracle.decide(n, dur, devmask, mem, edges, order, lo, hi, ndev, init_mem, cap,
+                         node_budget, 0.0)

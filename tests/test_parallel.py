@@ -1,0 +1,140 @@
+"""CPU tests of the host-side search logic and the multi-rank protocol.
+
+The native engine and the decide seam are replaced by oracle-backed stand-ins
+(tests/cpu_engine.py) so that the level-synchronous scan, deferral stages,
+retirement limits, ordered replay, candidate log and the world_size-2 gloo
+sharding (parallel.py) run here and must reproduce the reference's goldens
+bit-exactly."""
+
+import json
+import os
+import socket
+import sys
+import tempfile
+from pathlib import Path
+
+import pytest
+
+from conftest import GOLDEN, ROOT, load_search
+
+CASES = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "k4_k3", "m4_cap8", "C1", "v2_k4"]
+
+
+def _patch_decide(monkeypatch):
+    from cpu_engine import oracle_decide
+
+    import paper_2311_15269_b200._core as core
+
+    monkeypatch.setattr(core, "decide", oracle_decide)
+
+
+def _run(name, comm=None, small_windows=False):
+    import paper_2311_15269_b200.completion as C
+    import paper_2311_15269_b200.engine as E
+    from cpu_engine import OracleEngine
+    from paper_2311_15269_b200.placement import placement_from_dict
+
+    doc = load_search(name)
+    p = placement_from_dict(doc["placement"])
+    eng = E.BatchedRepetendSearch(p, native=OracleEngine(p))
+    if small_windows:  # many windows + many levels per window
+        C.WINDOW_FIRST, C.WINDOW_GROWTH = 3, 2
+        eng.small_budget = 2
+        eng.resolve_stages = ((0, 8), (0, 0))
+    try:
+        res = C.search(p, doc["mem_capacity"], max_nr=doc["max_nr"], engine=eng, comm=comm)
+    finally:
+        C.WINDOW_FIRST, C.WINDOW_GROWTH = E.WINDOW_FIRST, E.WINDOW_GROWTH
+    return doc, res
+
+
+def _summary(res):
+    s = res.schedule
+    return {
+        "best_t_r": res.report.best_t_r,
+        "improvements": [[list(a), t] for a, t in res.report.improvements],
+        "n_candidates": len(res.report.candidates),
+        "entries": sorted([b.stage, b.mb, t] for b, t in s.entries.items()),
+        "repetend": [s.repetend.start, s.repetend.end, s.repetend.period, s.repetend.nr],
+        "counts": dict(res.report.candidates.counts),
+        "records": [[c.n_r, list(c.assignment), c.t_r, c.status] for c in res.report.candidates
+                    if c.status != "bound"],
+        "diagnostics": res.report.diagnostics,
+    }
+
+
+def _expected(doc):
+    return {
+        "best_t_r": doc["best_t_r"], "improvements": doc["improvements"],
+        "n_candidates": doc["n_candidates"], "entries": doc["schedule"]["entries"],
+        "repetend": doc["schedule"]["repetend"], "counts": doc["status_counts"],
+        "records": doc["records"], "diagnostics": doc["diagnostics"],
+    }
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("small", [False, True])
+def test_level_scan_and_replay_match_reference(monkeypatch, name, small):
+    """Single shard: the GPU engine's host logic over the oracle stand-in."""
+    _patch_decide(monkeypatch)
+    doc, res = _run(name, small_windows=small)
+    assert _summary(res) == _expected(doc)
+
+
+def _worker(rank, world, port, names, out_dir):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        import paper_2311_15269_b200._core as core
+        from cpu_engine import oracle_decide
+        from paper_2311_15269_b200.parallel import Comm
+
+        core.decide = oracle_decide
+        comm = Comm()
+        for name in names:
+            for small in (False, True):
+                _, res = _run(name, comm=comm, small_windows=small)
+                Path(out_dir, f"{name}_{small}_{rank}.json").write_text(
+                    json.dumps(_summary(res)))
+        Path(out_dir, f"collectives_{rank}.txt").write_text(str(comm.collectives))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_two_rank_sharded_search_matches_reference():
+    """world_size 2 (gloo): windows split by rank prefix, one all-reduce-min
+    per level, all-gathered SAT rows, identical replay on both ranks."""
+    import torch.multiprocessing as mp
+
+    names = ["x4_demo_k3", "k4_k3", "m4_cap8", "v4_unit_cap4"]
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_worker, args=(2, _free_port(), names, out), nprocs=2, join=True)
+        for name in names:
+            exp = _expected(load_search(name))
+            for small in (False, True):
+                r0 = json.loads(Path(out, f"{name}_{small}_0.json").read_text())
+                r1 = json.loads(Path(out, f"{name}_{small}_1.json").read_text())
+                assert r0 == r1 == exp, (name, small)
+        assert int(Path(out, "collectives_0.txt").read_text()) > 0
+
+
+def test_split_range_covers_window():
+    from paper_2311_15269_b200.parallel import split_range
+
+    for n in (0, 1, 5, 17, 1000):
+        for g in (1, 2, 3, 8):
+            parts = [split_range(10, 10 + n, r, g) for r in range(g)]
+            assert parts[0][0] == 10 and parts[-1][1] == 10 + n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(g - 1))
