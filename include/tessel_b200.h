@@ -144,6 +144,22 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
                        int32_t *sat_starts, int64_t *out_active, int64_t *out_deferred,
                        tsl_level_stats *stats);
 
+/* Speculation support (see engine.py): take the deferred entries of the last
+ * stage with window index <= widx_limit to the host (ascending; they leave
+ * the device lists unsettled), and append window indices to the active list
+ * (probed again at the next period). */
+int tsl_engine_take_deferred(tsl_engine *e, int64_t widx_limit, int64_t max_out,
+                             int64_t *widx_out, int64_t *out_count);
+int tsl_engine_add_active(tsl_engine *e, int64_t count, const int64_t *widx);
+
+/* Reference-exact repetend probes for explicit (window index, period) pairs
+ * of the staged window, each under its own node cap (0 = none), run
+ * concurrently (one warp per pair).  Writes status, node count and, on SAT,
+ * starts[i*K .. +K). */
+int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const int32_t *period,
+                      const int64_t *node_budget, int64_t cap, int32_t *status_out,
+                      int64_t *nodes_out, int32_t *starts_out);
+
 /* Rows [first, first+count) of the last probe's SAT list (ascending window
  * index): window indices and starts[count*K].  Rows stay on the device until
  * the next tsl_engine_probe / tsl_engine_stage call. */

@@ -82,7 +82,8 @@ EXPORTS = (
     "tsl_last_error", "tsl_version", "tsl_device_count", "tsl_set_device", "tsl_decide",
     "tsl_decide_batch", "tsl_engine_open", "tsl_engine_close", "tsl_engine_count",
     "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
-    "tsl_engine_sat_rows",
+    "tsl_engine_sat_rows", "tsl_engine_take_deferred", "tsl_engine_add_active",
+    "tsl_engine_verify",
     "tsl_engine_last_kernel_ms", "tsl_counters",
 )
 
@@ -119,6 +120,12 @@ def lib():
     L.tsl_engine_resolve.restype = i32
     L.tsl_engine_resolve.argtypes = [vp, i32, i64, i64, i64, i64, i64, dbl, i64, vp, vp, vp,
                                      vp, vp, vp]
+    L.tsl_engine_take_deferred.restype = i32
+    L.tsl_engine_take_deferred.argtypes = [vp, i64, i64, vp, vp]
+    L.tsl_engine_add_active.restype = i32
+    L.tsl_engine_add_active.argtypes = [vp, i64, vp]
+    L.tsl_engine_verify.restype = i32
+    L.tsl_engine_verify.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp, vp]
     L.tsl_engine_sat_rows.restype = i32
     L.tsl_engine_sat_rows.argtypes = [vp, i64, i64, vp, vp]
     L.tsl_counters.restype = None
@@ -298,6 +305,34 @@ class Engine:
         k = min(n, max_sat)
         return (n, widx[:k].copy(), rows[:k * self.K].reshape(k, self.K).copy(), int(n_act[0]),
                 int(n_def[0]), {f: getattr(st, f) for f, _ in _Stats._fields_})
+
+    def take_deferred(self, widx_limit: int, max_out: int):
+        out = np.zeros(max(max_out, 1), dtype=np.int64)
+        n = np.zeros(1, dtype=np.int64)
+        check(self._L.tsl_engine_take_deferred(self._h, int(widx_limit), int(max_out),
+                                               _ptr(out), _ptr(n)))
+        return out[:int(n[0])].copy()
+
+    def add_active(self, widx):
+        a = np.ascontiguousarray(widx, dtype=np.int64)
+        if a.size:
+            check(self._L.tsl_engine_add_active(self._h, int(a.size), _ptr(a)))
+
+    def verify(self, widx, periods, budgets, cap):
+        """Exact probes for explicit (widx, period) pairs ->
+        (status[], nodes[], starts[count, K])."""
+        w = np.ascontiguousarray(widx, dtype=np.int64)
+        per = np.ascontiguousarray(periods, dtype=np.int32)
+        bud = np.ascontiguousarray(budgets, dtype=np.int64)
+        n = int(w.size)
+        st = np.zeros(max(n, 1), dtype=np.int32)
+        nd = np.zeros(max(n, 1), dtype=np.int64)
+        rows = np.zeros(max(n, 1) * self.K, dtype=np.int32)
+        if n:
+            check(self._L.tsl_engine_verify(self._h, n, _ptr(w), _ptr(per), _ptr(bud),
+                                            -1 if cap is None else int(cap), _ptr(st), _ptr(nd),
+                                            _ptr(rows)))
+        return st[:n].copy(), nd[:n].copy(), rows[:n * self.K].reshape(n, self.K).copy()
 
     def sat_rows(self, first: int, count: int):
         widx = np.zeros(max(count, 1), dtype=np.int64)

@@ -428,6 +428,47 @@ __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gp
   }
 }
 
+// Verification of speculated probes: explicit (window index, period)
+// pairs, one warp each, reference-exact DFS under the reference cap for that
+// period (0 = none at the load bound).  Writes status / nodes / starts per
+// pair (no list compaction: the host owns the bookkeeping).
+__global__ void __launch_bounds__(128) k_verify_warp(const int *__restrict__ gpool,
+                                                     const unsigned char *__restrict__ assign,
+                                                     const int *__restrict__ vwidx,
+                                                     const int *__restrict__ vper,
+                                                     const long long *__restrict__ vbudget,
+                                                     int count, int cap, int *vstatus,
+                                                     long long *vnodes, int *vstarts) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int per_warp = rep_warp_smem_words(sp);
+  int *mine_s = sp + ((sp[R_WORDS] + 3) & ~3) + wib * ((per_warp + 3) & ~3);
+  const int ndep1 = sp[R_NDEP] > 0 ? sp[R_NDEP] : 1;
+  int *snap = mine_s + ((wrx_state_words(K, sp[R_MAXDI]) + 3) & ~3);
+  int *deplag = snap + (int)wrx_snap_words(K);
+  int *init = deplag + ndep1;
+  WWs w = wrx_carve(mine_s, snap, K, sp[R_MAXDI]);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + wib; t < count; t += nwarps) {
+    const int P = vper[t];
+    const unsigned char *a = assign + (long long)vwidx[t] * K;
+    if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
+    __syncwarp();
+    const RepView v = rep_view(sp, P, cap, deplag, init);
+    long long nd = 0;
+    const int st = wrx_decide(v, w, vbudget[t], 0ull, &nd);
+    if (lane == 0) {
+      vstatus[t] = st;
+      vnodes[t] = nd;
+    }
+    if (st == RX_SAT)
+      for (int i = lane; i < K; i += 32) vstarts[t * K + i] = w.s[i];
+    __syncwarp();
+  }
+}
+
 __global__ void k_gather_rows(const int *__restrict__ rows, const int *__restrict__ pos, int count,
                               int K, int *__restrict__ out) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -600,6 +641,8 @@ struct tsl_engine {
   std::vector<int> sat_widx_sorted, sat_pos_sorted;
   int *d_gather = nullptr;
   size_t d_gather_cap = 0;
+  char *d_verify = nullptr;
+  size_t d_verify_cap = 0;
   // per-thread DFS scratch
   int *d_ws = nullptr;
   long long ws_words = 0;
@@ -687,7 +730,7 @@ struct tsl_engine {
     for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
                     (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather,
-                    (void *)d_def[0], (void *)d_def[1]})
+                    (void *)d_def[0], (void *)d_def[1], (void *)d_verify})
       if (p) cudaFree(p);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -1012,6 +1055,104 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
   *out_deferred = counters[2];
   fill_stats(st, stats);
   return finish_level(e, counters[1], max_sat, out_nsat, sat_widx, sat_starts);
+  API_END
+}
+
+// Take the deferred list of the last stage (entries <= widx_limit) to the
+// host without settling it; the entries leave the device lists.
+int tsl_engine_take_deferred(tsl_engine *e, int64_t widx_limit, int64_t max_out,
+                             int64_t *widx_out, int64_t *out_count) {
+  API_BEGIN
+  const long long n = e->n_def;
+  std::vector<int> buf(n);
+  if (n > 0) {
+    d2h(buf.data(), e->d_def[e->dcur], n * sizeof(int), e->stream);
+    CK(cudaStreamSynchronize(e->stream));
+  }
+  std::sort(buf.begin(), buf.end());
+  long long k = 0;
+  for (long long i = 0; i < n; ++i)
+    if (buf[i] <= widx_limit) {
+      if (k >= max_out) throw tsl::Error(TSL_EINVAL, "take_deferred: output too small");
+      widx_out[k++] = buf[i];
+    }
+  e->n_def = 0;
+  *out_count = k;
+  return TSL_OK;
+  API_END
+}
+
+// Append window indices to the active list (they are probed at the next
+// level like any other active candidate).
+int tsl_engine_add_active(tsl_engine *e, int64_t count, const int64_t *widx) {
+  API_BEGIN
+  if (count <= 0) return TSL_OK;
+  if (e->n_act + count > e->W_cap) throw tsl::Error(TSL_EINVAL, "active list overflow");
+  std::vector<int> buf(widx, widx + count);
+  h2d(e->d_act[e->cur] + e->n_act, buf.data(), count * sizeof(int), e->stream);
+  CK(cudaStreamSynchronize(e->stream));
+  e->n_act += count;
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const int32_t *period,
+                      const int64_t *node_budget, int64_t cap, int32_t *status_out,
+                      int64_t *nodes_out, int32_t *starts_out) {
+  API_BEGIN
+  if (!e->gpu_ready) throw tsl::Error(TSL_EINVAL, "tsl_engine_verify before tsl_engine_stage");
+  if (count <= 0) return TSL_OK;
+  CK(cudaSetDevice(e->device));
+  const int K = e->pool[R_K];
+  const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
+  std::vector<int> w32(count), p32(count);
+  for (long long i = 0; i < count; ++i) {
+    if (widx[i] < 0 || widx[i] >= e->W) throw tsl::Error(TSL_EINVAL, "verify: bad window index");
+    tsl::ck(2LL * (K - 1) * ((long long)period[i] + e->pool[R_MAXDUR]) + 4LL * e->pool[R_TOTAL],
+            "period anchor");
+    w32[i] = (int)widx[i];
+    p32[i] = period[i];
+  }
+  const size_t b_i = ((size_t)count * sizeof(int) + 255) / 256 * 256;
+  const size_t b_l = ((size_t)count * sizeof(long long) + 255) / 256 * 256;
+  const size_t need = 3 * b_i + 2 * b_l + (size_t)count * K * sizeof(int);
+  if (need > e->d_verify_cap) {
+    if (e->d_verify) CK(cudaFree(e->d_verify));
+    CK(cudaMalloc(&e->d_verify, need));
+    e->d_verify_cap = need;
+  }
+  char *q = e->d_verify;
+  int *d_w = (int *)q; q += b_i;
+  int *d_p = (int *)q; q += b_i;
+  int *d_st = (int *)q; q += b_i;
+  long long *d_b = (long long *)q; q += b_l;
+  long long *d_n = (long long *)q; q += b_l;
+  int *d_s = (int *)q;
+  h2d(d_w, w32.data(), count * sizeof(int), e->stream);
+  h2d(d_p, p32.data(), count * sizeof(int), e->stream);
+  h2d(d_b, node_budget, count * sizeof(long long), e->stream);
+  const int wpb = 4;
+  const size_t smem = (size_t)(((e->pool.size() + 3) & ~(size_t)3) +
+                               wpb * ((rep_warp_smem_words(e->pool.data()) + 3) & ~3)) *
+                      sizeof(int);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_verify_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  long long blocks = (count + wpb - 1) / wpb;
+  blocks = std::min<long long>(blocks, (long long)e->num_sms * 16);
+  CK(cudaEventRecord(e->ev0, e->stream));
+  COUNT_LAUNCH();
+  k_verify_warp<<<(int)blocks, 32 * wpb, smem, e->stream>>>(e->d_pool, e->d_assign, d_w, d_p,
+                                                             d_b, (int)count, icap, d_st, d_n,
+                                                             d_s);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e->ev1, e->stream));
+  d2h(status_out, d_st, count * sizeof(int), e->stream);
+  d2h(nodes_out, d_n, count * sizeof(long long), e->stream);
+  d2h(starts_out, d_s, (size_t)count * K * sizeof(int), e->stream);
+  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
+  return TSL_OK;
   API_END
 }
 

@@ -45,6 +45,9 @@ DJ_BUDGET = 200_000   # disjunctive-refutation nodes per deferred probe
 # reference cap).  The retirement limit is re-applied between stages, so a
 # probe above the lowest completion-feasible SAT never runs the full cap.
 RESOLVE_STAGES = ((DJ_BUDGET, 32_768), (0, 0))
+# with speculation the last (reference-cap) stage is replaced by pending
+# probes verified once per window
+SPEC_STAGES = ((DJ_BUDGET, 32_768),)
 TRACE = os.environ.get("TESSEL_TRACE", "0") == "1"
 
 
@@ -61,6 +64,8 @@ class EngineCounters:
     deferred: int = 0
     dj_refuted: int = 0
     dj_nodes: int = 0
+    verified: int = 0        # speculated probes verified at window ends
+    redo: int = 0            # window rescans after a misprediction
     kernel_ms: float = 0.0
     probe_ms: float = 0.0     # k_probe (first pass)
     resolve_ms: float = 0.0   # k_resolve_warp (DJ + warp RX-DFS stages)
@@ -112,11 +117,14 @@ class BatchedRepetendSearch:
         self.total = sum(dur)
         self.counters = EngineCounters()
         self.small_budget = SMALL_BUDGET
-        self.resolve_stages = RESOLVE_STAGES
+        self.speculate = os.environ.get("TESSEL_SPECULATE", "1") == "1"
+        self.resolve_stages = SPEC_STAGES if self.speculate else RESOLVE_STAGES
 
-    def _scan_sats(self, res, n_r, r0, period, n_sat, widx, rows, limit, feasible):
-        """Walk the level's SAT rows in window order up to the first
+    def _scan_sats(self, res, n_r, r0, period, n_sat, widx, rows, limit, feasible, extra=()):
+        """Walk the level's SAT rows (device list, already sorted, merged with
+        host-known SATs `extra`) in window order up to the first
         completion-feasible one; it retires every higher index."""
+        dev = []
         i, start = 0, 0
         while i < n_sat:
             if i >= start + len(widx):
@@ -126,11 +134,15 @@ class BatchedRepetendSearch:
             w = int(widx[j])
             if w > limit:
                 break
-            res.first_sat[w] = (period, rows[j].copy())
-            if feasible(n_r, r0 + w, period, rows[j]):
+            dev.append((w, rows[j]))
+            i += 1
+        for w, row in sorted(list(extra) + dev, key=lambda r: r[0]):
+            if w > limit:
+                break
+            res.first_sat[w] = (period, np.array(row, dtype=np.int32).copy())
+            if feasible(n_r, r0 + w, period, row):
                 res.first_feasible = w
                 return w - 1
-            i += 1
         return limit
 
     def count(self, n_r: int) -> int:
@@ -148,10 +160,47 @@ class BatchedRepetendSearch:
         """Level-synchronous period scan of ranks [r0, r1) at n_r under the
         sequential bound ``bound`` in force at the window start.
         ``feasible(n_r, rank, period, starts)`` is the completion check.
-        ``sync(first_feasible, limit, n_active) -> (limit, any_active)``
-        exchanges the retirement bound with the other shards of the window
-        (parallel.LevelSync); None = single shard."""
+        ``sync`` (parallel.LevelSync) exchanges the retirement bound with the
+        other shards of the window; None = single shard.
+
+        Speculation: deferred probes that survive the disjunctive filter and
+        the 32k-node stage would need the reference's full 400k-node cap, one
+        launch per level.  They are instead assumed "not SAT" (the outcome for
+        nearly all of them), the scan continues, and all pending probes of the
+        window are verified together in ONE launch at the end.  If any turns
+        out SAT the window is scanned again with every verified outcome as a
+        hint, so the final result is exactly the sequential one."""
+        hints: dict = {}
+        for _ in range(1 + 4 * 64):
+            res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, sync,
+                                             hints)
+            if res.timed_out:
+                return res
+            mispredicted = False
+            if pending:
+                w = [x for x, _ in pending]
+                per = [q for _, q in pending]
+                bud = [0 if q == self.lb else PROBE_NODES for q in per]
+                st, nodes, rows = self.eng.verify(w, per, bud, cap)
+                self.counters.add({"probes": 0, "root_refuted": 0, "nodes": int(nodes.sum()),
+                                   "capped": int((st == _native.TIMEOUT).sum()),
+                                   "sat": int((st == _native.SAT).sum()), "deferred": 0,
+                                   "dj_refuted": 0, "dj_nodes": 0},
+                                  self.eng.last_kernel_ms(), False, (n_r, r0, 0, "verify"))
+                self.counters.verified += len(w)
+                for i, (x, q) in enumerate(pending):
+                    hints[(x, q)] = (int(st[i]), rows[i].copy())
+                    mispredicted |= int(st[i]) == _native.SAT
+            if sync is not None:
+                mispredicted = sync.any(mispredicted)
+            if not mispredicted:
+                return res
+            self.counters.redo += 1
+        raise RuntimeError("speculation did not converge")
+
+    def _scan_window(self, n_r, r0, r1, cap, bound, feasible, deadline, sync, hints):
         res = WindowResult(n_r, r0, r1 - r0)
+        pending = []
         n_act, gate = self.eng.stage(n_r, r0, r1, cap, want_gate=cap is not None)
         self.counters.windows += 1
         self.counters.launches += 1  # k_stage
@@ -171,7 +220,7 @@ class BatchedRepetendSearch:
                 left = deadline - time.monotonic()
                 if left <= 0:
                     res.timed_out = True
-                    return res
+                    return res, pending
                 budget_secs = left
             node_cap = 0 if period == self.lb else PROBE_NODES
             n_sat, widx, rows, n_act, n_def, st = self.eng.probe(
@@ -179,7 +228,7 @@ class BatchedRepetendSearch:
             self.counters.add(st, self.eng.last_kernel_ms(), True, (n_r, r0, period, "probe"))
             if deadline and st["capped"] and time.monotonic() > deadline:
                 res.timed_out = True
-                return res
+                return res, pending
             limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit, feasible)
             for dj_budget, stage_budget in self.resolve_stages:
                 if not n_def:
@@ -191,10 +240,27 @@ class BatchedRepetendSearch:
                                   (n_r, r0, period, f"resolve{stage_budget}"))
                 if deadline and st["capped"] and time.monotonic() > deadline:
                     res.timed_out = True
-                    return res
+                    return res, pending
                 limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit,
                                         feasible)
+            if self.speculate and n_def:
+                spec, known_sat, back = [], [], []
+                for w in self.eng.take_deferred(limit, n_def):
+                    h = hints.get((int(w), period))
+                    if h is None:
+                        spec.append(int(w))
+                        back.append(int(w))
+                    elif h[0] == _native.SAT:
+                        known_sat.append((int(w), h[1]))
+                    else:
+                        back.append(int(w))
+                self.eng.add_active(back)
+                n_act += len(back)
+                if known_sat:
+                    limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit,
+                                            feasible, extra=known_sat)
+                pending += [(w, period) for w in spec if w <= limit]
             active = n_act > 0
             if sync is not None:
                 limit, active = sync(res.first_feasible, limit, n_act)
-        return res
+        return res, pending

@@ -84,3 +84,7 @@ class LevelSync:
         if g_first < BIG:
             limit = min(limit, g_first - self.offset - 1)
         return limit, -neg_active > 0
+
+    def any(self, flag: bool) -> bool:
+        """True on every rank if any rank raised `flag` (speculation verdicts)."""
+        return self.comm.allreduce_min([-int(bool(flag))])[0] < 0

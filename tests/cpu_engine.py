@@ -108,6 +108,24 @@ class OracleEngine:
         n, widx, rows = self._rows(max_sat)
         return n, widx, rows, len(self.active), len(redo), st
 
+    def take_deferred(self, widx_limit, max_out):
+        out = sorted(w for w in self.deferred if w <= widx_limit)
+        self.deferred = []
+        return np.array(out, dtype=np.int64)
+
+    def add_active(self, widx):
+        self.active.extend(int(w) for w in widx)
+
+    def verify(self, widx, periods, budgets, cap):
+        st, nodes, rows = [], [], []
+        for w, per, b in zip(widx, periods, budgets):
+            s, starts, nd = self._probe(int(w), int(per), cap, int(b))
+            st.append(s)
+            nodes.append(nd)
+            rows.append(starts if starts is not None else [0] * self.K)
+        return (np.array(st, dtype=np.int32), np.array(nodes, dtype=np.int64),
+                np.array(rows, dtype=np.int32).reshape(len(st), self.K))
+
     def sat_rows(self, first, count):
         self.sats.sort(key=lambda r: r[0])
         part = self.sats[first:first + count]

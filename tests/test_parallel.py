@@ -28,7 +28,7 @@ def _patch_decide(monkeypatch):
     monkeypatch.setattr(core, "decide", oracle_decide)
 
 
-def _run(name, comm=None, small_windows=False):
+def _run(name, comm=None, small_windows=False, speculate=True):
     import paper_2311_15269_b200.completion as C
     import paper_2311_15269_b200.engine as E
     from cpu_engine import OracleEngine
@@ -37,10 +37,12 @@ def _run(name, comm=None, small_windows=False):
     doc = load_search(name)
     p = placement_from_dict(doc["placement"])
     eng = E.BatchedRepetendSearch(p, native=OracleEngine(p))
-    if small_windows:  # many windows + many levels per window
+    eng.speculate = speculate
+    eng.resolve_stages = E.SPEC_STAGES if speculate else E.RESOLVE_STAGES
+    if small_windows:  # many windows, many levels, many deferrals / speculations
         C.WINDOW_FIRST, C.WINDOW_GROWTH = 3, 2
         eng.small_budget = 2
-        eng.resolve_stages = ((0, 8), (0, 0))
+        eng.resolve_stages = ((0, 8),) if speculate else ((0, 8), (0, 0))
     try:
         res = C.search(p, doc["mem_capacity"], max_nr=doc["max_nr"], engine=eng, comm=comm)
     finally:
@@ -74,11 +76,25 @@ def _expected(doc):
 
 @pytest.mark.parametrize("name", CASES)
 @pytest.mark.parametrize("small", [False, True])
-def test_level_scan_and_replay_match_reference(monkeypatch, name, small):
-    """Single shard: the GPU engine's host logic over the oracle stand-in."""
+@pytest.mark.parametrize("speculate", [True, False])
+def test_level_scan_and_replay_match_reference(monkeypatch, name, small, speculate):
+    """Single shard: the GPU engine's host logic over the oracle stand-in,
+    with and without speculation of full-cap probes."""
     _patch_decide(monkeypatch)
-    doc, res = _run(name, small_windows=small)
+    doc, res = _run(name, small_windows=small, speculate=speculate)
     assert _summary(res) == _expected(doc)
+
+
+def test_speculation_mispredictions_are_repaired(monkeypatch):
+    """Tiny budgets make many probes pending; some verify SAT, forcing window
+    rescans — the result must still be exact."""
+    _patch_decide(monkeypatch)
+    redo = 0
+    for name in CASES:
+        doc, res = _run(name, small_windows=True, speculate=True)
+        assert _summary(res) == _expected(doc)
+        redo += res.report.engine["redo"]
+    assert redo > 0
 
 
 def _worker(rank, world, port, names, out_dir):
