@@ -38,6 +38,17 @@ inline int ck(long long v, const char *what) {
 
 inline int popcount64(uint64_t x) { return __builtin_popcountll(x); }
 
+// 1 per node whose CSR list names the same target more than once
+inline std::vector<int> dup_flags(const std::vector<int> &ptr, const std::vector<int> &dst, int n) {
+  std::vector<int> out(n > 0 ? n : 1, 0);
+  for (int a = 0; a < n; ++a) {
+    std::vector<int> t(dst.begin() + ptr[a], dst.begin() + ptr[a + 1]);
+    std::sort(t.begin(), t.end());
+    out[a] = std::adjacent_find(t.begin(), t.end()) != t.end();
+  }
+  return out;
+}
+
 // ------------------------------------------------------------------ GenView
 inline std::vector<int> gen_build(int n, const int64_t *dur, const uint64_t *devmask,
                                   const int64_t *mem, const int64_t *edges, int m,
@@ -142,6 +153,8 @@ inline std::vector<int> gen_build(int n, const int64_t *dur, const uint64_t *dev
   put(dev_items);
   put(devof_ptr);
   put(devof);
+  put(dup_flags(out_ptr, out_dst, n));
+  put(dup_flags(in_ptr, in_src, n));
   pool[G_WORDS] = (int)pool.size();
   return pool;
 }
@@ -325,6 +338,8 @@ inline std::vector<int> rep_build(const Placement &pl) {
   put(R_PDEVPTR, pdev_ptr);
   put(R_PDEV, pdev);
   put(R_DEVNPAIR, devnpair);
+  put(R_OUTDUP, dup_flags(out_ptr, out_dst, K));
+  put(R_INDUP, dup_flags(in_ptr, in_src, K));
   put(R_LSPTR, ls_ptr);
   put(R_LS, ls);
   put(R_HSPTR, hs_ptr);

@@ -20,8 +20,11 @@ struct GenView {
   const int *dur_, *mem_, *order_, *lo_, *hi_, *init_;
   const int *out_ptr_, *out_dst_, *out_lag_, *in_ptr_, *in_src_, *in_lag_;
   const int *conf_ptr_, *conf_dst_, *dev_ptr_, *dev_items_, *devof_ptr_, *devof_;
+  const int *out_dup_, *in_dup_;  // 1 if the node's edge list repeats a target
 
   RX_HD int n() const { return n_; }
+  RX_HD bool out_dup(int a) const { return out_dup_[a] != 0; }
+  RX_HD bool in_dup(int a) const { return in_dup_[a] != 0; }
   RX_HD int ndev() const { return ndev_; }
   RX_HD int cap() const { return cap_; }
   RX_HD int dur(int i) const { return dur_[i]; }
@@ -79,7 +82,9 @@ RX_HD GenView gen_view(const int *pool) {
   g.dev_ptr_ = p; p += ndev + 1;
   g.dev_items_ = p; p += nmemb;
   g.devof_ptr_ = p; p += n + 1;
-  g.devof_ = p;
+  g.devof_ = p; p += nmemb;
+  g.out_dup_ = p; p += n;
+  g.in_dup_ = p;
   return g;
 }
 
@@ -94,7 +99,7 @@ enum {
   R_DEVOF,
   // disjunctive pairs {x < y} of items with intersecting device masks, the
   // devices each pair shares, and the number of pairs per device
-  R_PAIRX, R_PAIRY, R_PDEVPTR, R_PDEV, R_DEVNPAIR,
+  R_PAIRX, R_PAIRY, R_PDEVPTR, R_PDEV, R_DEVNPAIR, R_OUTDUP, R_INDUP,
   // enumeration metadata: per stage st, lo sources (succ j < st), hi
   // sources (pred i < st), and the frontier F_{st+1} after assigning st
   R_LSPTR, R_LS, R_HSPTR, R_HS, R_FRPTR, R_FR,
@@ -110,12 +115,15 @@ struct RepView {
   const int *dur_, *mem_, *order_, *out_ptr_, *out_dst_, *out_row_, *out_dep_end_;
   const int *in_ptr_, *in_src_, *in_row_, *in_dep_end_, *in_srcdur_;
   const int *conf_ptr_, *conf_dst_, *dev_ptr_, *dev_items_, *devof_ptr_, *devof_;
+  const int *out_dup_, *in_dup_;
   const int *deplag;  // per dependency row: base - (a[src] - a[dst]) * P
   const int *init;    // entry memory per device
   int K, D, P, cap_;
 
   RX_HD int n() const { return K; }
   RX_HD int ndev() const { return D; }
+  RX_HD bool out_dup(int a) const { return out_dup_[a] != 0; }
+  RX_HD bool in_dup(int a) const { return in_dup_[a] != 0; }
   RX_HD int cap() const { return cap_; }
   RX_HD int dur(int i) const { return dur_[i]; }
   RX_HD int mem(int i) const { return mem_[i]; }
@@ -170,6 +178,8 @@ RX_HD RepView rep_view(const int *pool, int P, int cap, const int *deplag, const
   v.dev_items_ = pool + pool[R_DEVITEMS];
   v.devof_ptr_ = pool + pool[R_DEVOFPTR];
   v.devof_ = pool + pool[R_DEVOF];
+  v.out_dup_ = pool + pool[R_OUTDUP];
+  v.in_dup_ = pool + pool[R_INDUP];
   return v;
 }
 

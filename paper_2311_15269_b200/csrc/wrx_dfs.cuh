@@ -65,14 +65,21 @@ __device__ __forceinline__ bool wrx_bit(const unsigned *m, int i) {
 
 // Append the lanes flagged in `cand` (keys b) to the FIFO in lane order,
 // once per distinct b (its lowest flagged lane), setting their inq bits.
-__device__ __forceinline__ void wrx_enqueue(WWs &w, bool cand, int b, int n, int &qt, int &qc) {
+// `dedup` = the chunk may hold the same target twice (duplicated edge rows);
+// without it every candidate lane is its own leader (no __match_any_sync).
+__device__ __forceinline__ void wrx_enqueue(WWs &w, bool cand, int b, int n, int &qt, int &qc,
+                                            bool dedup = true) {
   const int lane = wrx_lane();
   __syncwarp();  // bound updates of this chunk visible before the next reads
   const unsigned candm = __ballot_sync(WRX_FULL, cand);
   if (!candm) return;
-  const unsigned grp = __match_any_sync(WRX_FULL, cand ? b : -1 - lane);
-  const bool leader = cand && (__ffs(grp) - 1 == lane);
-  const unsigned leadm = __ballot_sync(WRX_FULL, leader);
+  bool leader = cand;
+  unsigned leadm = candm;
+  if (dedup) {
+    const unsigned grp = __match_any_sync(WRX_FULL, cand ? b : -1 - lane);
+    leader = cand && (__ffs(grp) - 1 == lane);
+    leadm = __ballot_sync(WRX_FULL, leader);
+  }
   if (leader) {
     int slot = qt + __popc(leadm & ((1u << lane) - 1u));
     if (slot >= n) slot -= n;
@@ -118,7 +125,7 @@ __device__ bool wrx_propagate(const M &md, WWs &w, int &qh, int &qt, int &qc) {
         const bool imp = act && lane < f && nl > lob;
         __syncwarp();
         if (imp) atomicMax(&w.lo[b], nl);
-        wrx_enqueue(w, imp && !inq, b, n, qt, qc);
+        wrx_enqueue(w, imp && !inq, b, n, qt, qc, md.out_dup(a));
         if (failm) return false;
       }
     }
@@ -142,12 +149,133 @@ __device__ bool wrx_propagate(const M &md, WWs &w, int &qh, int &qt, int &qc) {
         const bool imp = act && lane < f && nh < hib;
         __syncwarp();
         if (imp) atomicMin(&w.hi[b], nh);
-        wrx_enqueue(w, imp && !inq, b, n, qt, qc);
+        wrx_enqueue(w, imp && !inq, b, n, qt, qc, md.in_dup(a));
         if (failm) return false;
       }
     }
   }
   return true;
+}
+
+
+// ---- warp sort / scan helpers (one element per lane, 32 lanes) --------
+__device__ __forceinline__ void wrx_bitonic(unsigned long long &key, int &p0, int &p1) {
+  const int lane = wrx_lane();
+  for (int size = 2; size <= 32; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const unsigned long long pk = __shfl_xor_sync(WRX_FULL, key, stride);
+      const int q0 = __shfl_xor_sync(WRX_FULL, p0, stride);
+      const int q1 = __shfl_xor_sync(WRX_FULL, p1, stride);
+      const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
+      const bool take = (lower == up) ? (pk < key) : (pk > key);
+      if (take) {
+        key = pk;
+        p0 = q0;
+        p1 = q1;
+      }
+    }
+  }
+}
+__device__ __forceinline__ int wrx_scan_add(int v) {  // inclusive prefix sum
+  const int lane = wrx_lane();
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(WRX_FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ int wrx_rscan_add(int v) {  // inclusive suffix sum
+  const int lane = wrx_lane();
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_down_sync(WRX_FULL, v, o);
+    if (lane + o < 32) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ int wrx_rscan_max(int v) {
+  const int lane = wrx_lane();
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_down_sync(WRX_FULL, v, o);
+    if (lane + o < 32) v = t > v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int wrx_scan_min(int v) {
+  const int lane = wrx_lane();
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(WRX_FULL, v, o);
+    if (lane >= o) v = t < v ? t : v;
+  }
+  return v;
+}
+// order-preserving 64-bit key from (value, tie) with value in (-2^30, 2^30)
+__device__ __forceinline__ unsigned long long wrx_key(int v, int tie) {
+  return ((unsigned long long)(unsigned)(v + (1 << 30)) << 32) | (unsigned)tie;
+}
+
+// _mem_ok for a device with k <= 32 items: sort events by time, prefix sums,
+// check the running sum at the end of every equal-time group.
+template <class M>
+__device__ bool wrx_mem_ok32(const M &md, WWs &w, int d, int cap, int pb, int k) {
+  const int lane = wrx_lane();
+  const int init = md.init_mem(d);
+  unsigned long long key = ~0ull;
+  int m = 0, dummy = 0;
+  if (lane < k) {
+    const int it = md.dev_item(pb + lane);
+    const int mm = md.mem(it);
+    const bool pl = wrx_bit(w.placed, it);
+    if (pl || mm < 0) {
+      key = wrx_key(pl ? w.s[it] : w.lo[it], lane);
+      m = mm;
+    }
+  }
+  wrx_bitonic(key, m, dummy);
+  const int run = init + wrx_scan_add(m);
+  const unsigned long long nkey = __shfl_down_sync(WRX_FULL, key, 1);
+  const bool valid = key != ~0ull;
+  const bool group_end = valid && (lane == 31 || nkey == ~0ull || (nkey >> 32) != (key >> 32));
+  return !__any_sync(WRX_FULL, group_end && run > cap);
+}
+
+// _dev_ok for a device with k <= 32 items: stable orders (a, position) and
+// (e, a-rank) by bitonic sorts; serial completion, suffix and prefix
+// energetic checks by scans.
+template <class M>
+__device__ bool wrx_dev_ok32(const M &md, WWs &w, int pb, int k) {
+  const int lane = wrx_lane();
+  const bool real = lane < k;
+  int a = 0, du = 0, e = -(1 << 30);
+  if (real) {
+    const int it = md.dev_item(pb + lane);
+    du = md.dur(it);
+    const bool pl = wrx_bit(w.placed, it);
+    a = pl ? w.s[it] : w.lo[it];
+    e = pl ? a + du : w.hi[it] + du;
+  }
+  const int lim = __reduce_max_sync(WRX_FULL, e);
+  const int sd = __reduce_add_sync(WRX_FULL, du);
+  unsigned long long key = real ? wrx_key(a, lane) : ~0ull;
+  int pd = du, pe = e;
+  wrx_bitonic(key, pd, pe);  // lane = rank in the stable a-order
+  const bool r2 = key != ~0ull;
+  const int ra = (int)(key >> 32) - (1 << 30);
+  const int suf_d = wrx_rscan_add(pd);
+  const int suf_e = wrx_rscan_max(pe);
+  bool bad = r2 && (ra + suf_d > suf_e);
+  int c = r2 ? ra + suf_d : sd;
+  c = __reduce_max_sync(WRX_FULL, c > sd ? c : sd);
+  bad |= c > lim;
+  // stable e-order of the a-sorted sequence: key (e, a-rank)
+  unsigned long long key2 = r2 ? wrx_key(pe, lane) : ~0ull;
+  int qa = r2 ? ra : (1 << 30), qd = r2 ? pd : 0;
+  wrx_bitonic(key2, qa, qd);
+  const bool r3 = key2 != ~0ull;
+  const int qe = (int)(key2 >> 32) - (1 << 30);
+  const int pre_d = wrx_scan_add(qd);
+  const int pre_a = wrx_scan_min(qa);
+  bad |= r3 && (pre_a + pre_d > qe);
+  return !__any_sync(WRX_FULL, bad);
 }
 
 // device checks ---------------------------------------------------------
@@ -159,6 +287,7 @@ __device__ bool wrx_mem_ok(const M &md, WWs &w, int d, int cap) {
   const int init = md.init_mem(d);
   if (init > cap) return false;
   const int pb = md.dev_begin(d), k = md.dev_end(d) - pb;
+  if (k > 8 && k <= 32) return wrx_mem_ok32(md, w, d, cap, pb, k);
   const int lane = wrx_lane();
   for (int i = lane; i < k; i += 32) {
     const int it = md.dev_item(pb + i);
@@ -188,6 +317,7 @@ template <class M>
 __device__ bool wrx_dev_ok(const M &md, WWs &w, int d) {
   const int pb = md.dev_begin(d), k = md.dev_end(d) - pb;
   if (k == 0) return true;
+  if (k > 8 && k <= 32) return wrx_dev_ok32(md, w, pb, k);
   const int lane = wrx_lane();
   int lim = -(1 << 30), sd = 0;
   for (int i = lane; i < k; i += 32) {
@@ -377,7 +507,7 @@ __device__ int wrx_decide(const M &md, WWs &w, long long budget, unsigned long l
         w.lo[y] = nlo;
         w.hi[y] = nhi;
       }
-      wrx_enqueue(w, chg && !inq, y, n, qt, qc);
+      wrx_enqueue(w, chg && !inq, y, n, qt, qc, false);  // conf lists are duplicate-free
     }
     if (ok) {
       ok = wrx_propagate(md, w, qh, qt, qc);
