@@ -204,6 +204,106 @@ __device__ __forceinline__ void emit_sat(const ProbeOut &o, int widx, const int 
   for (int i = 0; i < K; ++i) o.sat_starts[(long long)k * K + i] = s[i];
 }
 
+// K2a root filter, one warp per (candidate, P).  The reference's root step
+// (kernel_c.pyx:158-215) is FIFO bound propagation over the difference edges,
+// then _mem_ok / _dev_ok on every device; any failure is UNSAT with 0 nodes.
+// Its verdict does not depend on the propagation order: the propagation
+// reaches the unique greatest bounds-consistent box or fails iff that box is
+// empty.  Here the fixpoint is computed lane-parallel
+// (lanes over edge rows, atomicMax / atomicMin on shared bounds, rounds until
+// no lane changes a bound).  Without a positive cycle every bound settles
+// within K-1 rounds (longest simple path), so a change in round K+1 proves a
+// positive cycle, i.e. the propagation would push some lo above its hi.
+// At the root no item is placed, so _mem_ok's events are only negative
+// deltas and it reduces to init_d <= cap; _dev_ok runs the warp rank-based
+// check (wrx_dfs.cuh) per device.  Refuted probes stay active; survivors go
+// to k_probe's reference-exact DFS.
+__host__ __device__ inline int root_warp_words(const int *pool) {
+  const int K = pool[R_K];
+  return ((wrx_state_words(K, pool[R_MAXDI]) + 3) & ~3) + ((K + 3) & ~3);
+}
+
+__global__ void __launch_bounds__(256) k_root(const int *__restrict__ gpool,
+                                              const unsigned char *__restrict__ assign,
+                                              const int *__restrict__ act_in, int n_in,
+                                              ProbeOut o, int *__restrict__ surv, int P, int cap,
+                                              long long widx_limit) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K], D = sp[R_D], m = sp[R_M], ndep = sp[R_NDEP];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int *mine = sp + ((sp[R_WORDS] + 3) & ~3) + wib * root_warp_words(sp);
+  int *av = mine + ((wrx_state_words(K, sp[R_MAXDI]) + 3) & ~3);
+  WWs w = wrx_carve(mine, nullptr, K, sp[R_MAXDI]);
+  const int nw = (K + 31) / 32;
+  for (int i = lane; i < nw; i += 32) w.placed[i] = 0u;
+  const int *rsrc = sp + sp[R_RSRC], *rdst = sp + sp[R_RDST], *rbase = sp + sp[R_RBASE];
+  const int anchor = (K - 1) * (P + sp[R_MAXDUR]);
+  const RepView v = rep_view(sp, P, cap, nullptr, nullptr);
+  unsigned long long s_probe = 0, s_root = 0;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + wib; t < n_in; t += nwarps) {
+    const int widx = act_in[t];
+    if (widx > widx_limit) continue;  // retired by a lower-index completion-feasible SAT
+    const unsigned char *a = assign + (long long)widx * K;
+    for (int i = lane; i < K; i += 32) {
+      av[i] = a[i];
+      w.lo[i] = i == 0 ? anchor : 0;
+      w.hi[i] = i == 0 ? anchor : 2 * anchor;
+    }
+    __syncwarp();
+    bool fail = false;
+    if (cap >= 0) {  // root _mem_ok: init_d <= cap (entry memory, repetend.py:93-100)
+      bool bad = false;
+      for (int d = lane; d < D; d += 32) {
+        int e = 0;
+        for (int p = at_ptr(sp, R_DEVPTR, d); p < at_ptr(sp, R_DEVPTR, d + 1); ++p) {
+          const int st = sp[sp[R_DEVITEMS] + p];
+          e += av[st] * sp[sp[R_MEM] + st];
+        }
+        bad |= e > cap;
+      }
+      fail = __any_sync(WRX_FULL, bad);
+    }
+    for (int round = 0; !fail; ++round) {
+      bool changed = false;
+      for (int r = lane; r < m; r += 32) {
+        const int s = rsrc[r], d = rdst[r];
+        const int lag = rbase[r] - (r < ndep ? av[s] - av[d] : 1) * P;
+        const int nl = w.lo[s] + lag;
+        if (nl > w.lo[d]) {
+          atomicMax(&w.lo[d], nl);
+          changed = true;
+        }
+        const int nh = w.hi[d] - lag;
+        if (nh < w.hi[s]) {
+          atomicMin(&w.hi[s], nh);
+          changed = true;
+        }
+      }
+      __syncwarp();
+      bool bad = false;
+      for (int i = lane; i < K; i += 32) bad |= w.lo[i] > w.hi[i];
+      if (__any_sync(WRX_FULL, bad)) fail = true;
+      else if (!__any_sync(WRX_FULL, changed)) break;
+      else if (round >= K) fail = true;  // still moving after K+1 rounds: positive cycle
+    }
+    if (!fail)
+      for (int d = 0; d < D && !fail; ++d) fail = !wrx_dev_ok(v, w, d);
+    ++s_probe;
+    if (lane == 0) {
+      if (fail) o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
+      else surv[atomicAdd(&o.counters[3], 1)] = widx;
+    }
+    s_root += fail;
+    __syncwarp();
+  }
+  if (lane == 0 && s_probe) {
+    atomicAdd(&o.stats[0], s_probe);
+    atomicAdd(&o.stats[1], s_root);
+  }
+}
+
 // K2 level pass: probe (candidate, P) with a small node budget first.
 // Outcomes: SAT (exact: found within the small budget <= the reference cap),
 // UNSAT / TIMEOUT at the reference cap (exact "not SAT"), or DEFERRED (small
@@ -212,12 +312,17 @@ __device__ __forceinline__ void emit_sat(const ProbeOut &o, int widx, const int 
 __global__ void __launch_bounds__(128) k_probe(const int *__restrict__ gpool,
                                                const unsigned char *__restrict__ assign,
                                                const int *__restrict__ act_in, int n_in,
+                                               const int *__restrict__ n_in_dev,
                                                ProbeOut o, int P, long long full_budget,
                                                long long small_budget, int cap,
                                                long long widx_limit,
                                                unsigned long long budget_ns, int *ws_base,
                                                long long ws_words) {
   extern __shared__ int sp[];
+  // n_in_dev: survivors of k_root (already counted as probes there)
+  const bool counted = n_in_dev != nullptr;
+  if (counted) n_in = *n_in_dev;
+  if ((long long)blockIdx.x * blockDim.x >= n_in) return;
   load_pool(sp, gpool);
   const int K = sp[R_K];
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -255,7 +360,7 @@ __global__ void __launch_bounds__(128) k_probe(const int *__restrict__ gpool,
     }
   }
   if (s_probe) {
-    atomicAdd(&o.stats[0], s_probe);
+    if (!counted) atomicAdd(&o.stats[0], s_probe);
     atomicAdd(&o.stats[1], s_root);
     atomicAdd(&o.stats[2], s_nodes);
     atomicAdd(&o.stats[3], s_cap);
@@ -308,6 +413,11 @@ __global__ void __launch_bounds__(128) k_resolve(const int *__restrict__ gpool,
       o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
       continue;
     }
+    if (stage_budget < 0) {  // disjunctive filter only: undecided probes stay deferred
+      ++s_def;
+      o.def_out[atomicAdd(&o.counters[2], 1)] = widx;
+      continue;
+    }
     rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
     long long nd = 0;
     const int st = rx_decide(v, w, rx_budget, t_end, &nd);
@@ -344,6 +454,7 @@ __host__ __device__ inline int rep_warp_smem_words(const int *pool) {
 __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gpool,
                                                       const unsigned char *__restrict__ assign,
                                                       const int *__restrict__ def_in, int n_def,
+                                                      const int *__restrict__ n_def_dev,
                                                       ProbeOut o, int P, long long full_budget,
                                                       long long stage_budget,
                                                       long long dj_budget, int cap,
@@ -351,6 +462,9 @@ __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gp
                                                       unsigned long long budget_ns,
                                                       int *ws_base, long long ws_words) {
   extern __shared__ int sp[];
+  // n_def_dev: device-side count (k_root survivors; probes counted there)
+  if (n_def_dev) n_def = *n_def_dev;
+  if ((long long)blockIdx.x * (blockDim.x >> 5) >= n_def) return;
   load_pool(sp, gpool);
   const int K = sp[R_K];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -389,6 +503,14 @@ __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gp
         ++s_dju;
         o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
       }
+      continue;
+    }
+    if (stage_budget < 0) {  // disjunctive filter only: undecided probes stay deferred
+      if (lane == 0) {
+        ++s_def;
+        o.def_out[atomicAdd(&o.counters[2], 1)] = widx;
+      }
+      __syncwarp();
       continue;
     }
     if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
@@ -509,6 +631,13 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // TSL_DFS_MODE=thread selects the one-thread-per-probe DFS kernels (kept for
 // cross-validation); the default is the warp-cooperative DFS.
+// TSL_ROOT_FILTER=0 disables k_root (every probe runs k_probe's thread DFS;
+// kept for cross-validation).
+bool root_filter_off() {
+  const char *m = getenv("TSL_ROOT_FILTER");
+  return m && std::string(m) == "0";
+}
+
 bool decide_mode_warp() {
   const char *m = getenv("TSL_DFS_MODE");
   return !(m && std::string(m) == "thread");
@@ -631,6 +760,7 @@ struct tsl_engine {
   unsigned char *d_assign = nullptr, *d_gate = nullptr;
   int *d_act[2] = {nullptr, nullptr};
   int *d_def[2] = {nullptr, nullptr};
+  int *d_surv = nullptr;  // k_root survivors of the current level
   int dcur = 0;
   long long n_def = 0, n_sat = 0;
   int *d_sat_widx = nullptr, *d_sat_starts = nullptr;
@@ -711,7 +841,7 @@ struct tsl_engine {
     if (w <= W_cap) return;
     for (void *p : {(void *)d_assign, (void *)d_gate, (void *)d_act[0], (void *)d_act[1],
                     (void *)d_sat_widx, (void *)d_sat_starts, (void *)d_def[0],
-                    (void *)d_def[1]})
+                    (void *)d_def[1], (void *)d_surv})
       if (p) CK(cudaFree(p));
     const int K = pool[R_K];
     CK(cudaMalloc(&d_assign, (size_t)w * K));
@@ -720,6 +850,7 @@ struct tsl_engine {
     CK(cudaMalloc(&d_act[1], (size_t)w * sizeof(int)));
     CK(cudaMalloc(&d_def[0], (size_t)w * sizeof(int)));
     CK(cudaMalloc(&d_def[1], (size_t)w * sizeof(int)));
+    CK(cudaMalloc(&d_surv, (size_t)w * sizeof(int)));
     CK(cudaMalloc(&d_sat_widx, (size_t)w * sizeof(int)));
     CK(cudaMalloc(&d_sat_starts, (size_t)w * K * sizeof(int)));
     W_cap = w;
@@ -730,7 +861,7 @@ struct tsl_engine {
     for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
                     (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather,
-                    (void *)d_def[0], (void *)d_def[1], (void *)d_verify})
+                    (void *)d_def[0], (void *)d_def[1], (void *)d_verify, (void *)d_surv})
       if (p) cudaFree(p);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -966,10 +1097,44 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
   o.counters = e->d_counters;
   o.stats = e->d_stats;
   CK(cudaEventRecord(e->ev0, e->stream));
-  if (n_in > 0) {
+  if (n_in > 0 && !root_filter_off()) {
+    // K2a: warp-per-probe root filter, then the exact DFS on its survivors
+    const int wpb = 8;
+    const size_t smem = (size_t)(((e->pool.size() + 3) & ~(size_t)3) +
+                                 wpb * root_warp_words(e->pool.data())) * sizeof(int);
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_root, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    long long rblocks = (n_in + wpb - 1) / wpb;
+    rblocks = std::max(1LL, std::min<long long>(rblocks, (long long)e->num_sms * 8));
+    COUNT_LAUNCH();
+    k_root<<<(int)rblocks, 32 * wpb, smem, e->stream>>>(e->d_pool, e->d_assign,
+                                                        e->d_act[e->cur], (int)n_in, o,
+                                                        e->d_surv, period, icap, widx_limit);
+    CK(cudaGetLastError());
+    // survivors: warp-cooperative reference-exact DFS with the small budget
+    // (same outcome contract as k_probe: SAT / settled / deferred)
+    const int swpb = 4;
+    const size_t ssmem = (size_t)(((e->pool.size() + 3) & ~(size_t)3) +
+                                  swpb * ((rep_warp_smem_words(e->pool.data()) + 3) & ~3)) *
+                         sizeof(int);
+    if (ssmem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_resolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ssmem));
+    long long sblocks = (n_in + swpb - 1) / swpb;
+    sblocks = std::max(1LL, std::min<long long>(sblocks, (long long)e->ws_threads / (32 * swpb)));
+    const long long full = node_budget < 0 ? 0 : node_budget;
+    const long long sb = small_budget <= 0 ? 0 : small_budget;
+    // a probe is deferred only when the small budget is below the cap
+    const long long stage = (full == 0 || sb < full) ? sb : 0;
+    COUNT_LAUNCH();
+    k_resolve_warp<<<(int)sblocks, 32 * swpb, ssmem, e->stream>>>(
+        e->d_pool, e->d_assign, e->d_surv, 0, e->d_counters + 3, o, period, full, stage, 0,
+        icap, widx_limit, budget_ns, e->d_ws, e->ws_words);
+    CK(cudaGetLastError());
+  } else if (n_in > 0) {
     COUNT_LAUNCH();
     k_probe<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
-        e->d_pool, e->d_assign, e->d_act[e->cur], (int)n_in, o, period,
+        e->d_pool, e->d_assign, e->d_act[e->cur], (int)n_in, nullptr, o, period,
         node_budget < 0 ? 0 : node_budget, small_budget <= 0 ? 0 : small_budget, icap,
         widx_limit, budget_ns, e->d_ws, e->ws_words);
     CK(cudaGetLastError());
@@ -1030,15 +1195,15 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
                               (int)smem));
     COUNT_LAUNCH();
     k_resolve_warp<<<(int)wblocks, 32 * wpb, smem, e->stream>>>(
-        e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, o, period,
-        node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? 0 : stage_budget,
+        e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, nullptr, o, period,
+        node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? -1 : stage_budget,
         dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words);
     CK(cudaGetLastError());
   } else if (n_def > 0) {
     COUNT_LAUNCH();
     k_resolve<<<(int)blocks, threads, e->smem_bytes, e->stream>>>(
         e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, o, period,
-        node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? 0 : stage_budget,
+        node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? -1 : stage_budget,
         dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words);
     CK(cudaGetLastError());
   }

@@ -45,9 +45,10 @@ DJ_BUDGET = 200_000   # disjunctive-refutation nodes per deferred probe
 # reference cap).  The retirement limit is re-applied between stages, so a
 # probe above the lowest completion-feasible SAT never runs the full cap.
 RESOLVE_STAGES = ((DJ_BUDGET, 32_768), (0, 0))
-# with speculation the last (reference-cap) stage is replaced by pending
-# probes verified once per window
-SPEC_STAGES = ((DJ_BUDGET, 32_768),)
+# with speculation the RX-DFS stages are replaced by pending probes verified
+# once per window (one concurrent launch); -1 = disjunctive filter only.
+# TESSEL_SPEC_STAGE overrides the RX budget of the single resolve stage.
+SPEC_STAGES = ((DJ_BUDGET, int(os.environ.get("TESSEL_SPEC_STAGE", "32768"))),)
 TRACE = os.environ.get("TESSEL_TRACE", "0") == "1"
 
 
@@ -66,6 +67,7 @@ class EngineCounters:
     dj_nodes: int = 0
     verified: int = 0        # speculated probes verified at window ends
     redo: int = 0            # window rescans after a misprediction
+    repaired: int = 0        # mispredictions settled without a rescan
     kernel_ms: float = 0.0
     probe_ms: float = 0.0     # k_probe (first pass)
     resolve_ms: float = 0.0   # k_resolve_warp (DJ + warp RX-DFS stages)
@@ -97,6 +99,7 @@ class WindowResult:
     gate: Optional[np.ndarray] = None               # 1 = passes the memory gate
     timed_out: bool = False
     first_feasible: Optional[int] = None            # lowest completion-feasible SAT widx
+    retirers: set = field(default_factory=set)      # widx that lowered a retirement limit
 
 
 class BatchedRepetendSearch:
@@ -116,9 +119,10 @@ class BatchedRepetendSearch:
         self.lb = lower_bound(p)
         self.total = sum(dur)
         self.counters = EngineCounters()
-        self.small_budget = SMALL_BUDGET
+        self.small_budget = int(os.environ.get("TESSEL_SMALL_BUDGET", SMALL_BUDGET))
         self.speculate = os.environ.get("TESSEL_SPECULATE", "1") == "1"
         self.resolve_stages = SPEC_STAGES if self.speculate else RESOLVE_STAGES
+        self.repair = os.environ.get("TESSEL_REPAIR", "1") == "1"
 
     def _scan_sats(self, res, n_r, r0, period, n_sat, widx, rows, limit, feasible, extra=()):
         """Walk the level's SAT rows (device list, already sorted, merged with
@@ -142,6 +146,7 @@ class BatchedRepetendSearch:
             res.first_sat[w] = (period, np.array(row, dtype=np.int32).copy())
             if feasible(n_r, r0 + w, period, row):
                 res.first_feasible = w
+                res.retirers.add(w)
                 return w - 1
         return limit
 
@@ -163,13 +168,20 @@ class BatchedRepetendSearch:
         ``sync`` (parallel.LevelSync) exchanges the retirement bound with the
         other shards of the window; None = single shard.
 
-        Speculation: deferred probes that survive the disjunctive filter and
-        the 32k-node stage would need the reference's full 400k-node cap, one
-        launch per level.  They are instead assumed "not SAT" (the outcome for
-        nearly all of them), the scan continues, and all pending probes of the
-        window are verified together in ONE launch at the end.  If any turns
-        out SAT the window is scanned again with every verified outcome as a
-        hint, so the final result is exactly the sequential one."""
+        Speculation: deferred probes that survive the disjunctive filter
+        would need the reference-exact DFS up to the reference's 400k-node cap,
+        one latency-bound launch per level.  They are instead assumed "not
+        SAT" (the outcome for nearly all of them), the scan continues, and all
+        pending probes of the window are verified together in ONE launch at
+        the end.  A verified SAT (w, P) is a misprediction: w's first SAT is
+        P.  Every other outcome the scan recorded is a fact about its own
+        (candidate, period) and retirement only flows to higher indices, so
+        unless w itself lowered a retirement limit (its later SAT would not
+        exist in the exact scan) the window result is REPAIRED by recording
+        (P, row) as w's first SAT: candidates the exact scan would have
+        retired at P only carry first SATs at periods >= P, which the ordered
+        replay skips once w's period is the bound.  Otherwise the window is
+        scanned again with every verified outcome as a hint."""
         hints: dict = {}
         for _ in range(1 + 4 * 64):
             res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, sync,
@@ -177,6 +189,7 @@ class BatchedRepetendSearch:
             if res.timed_out:
                 return res
             mispredicted = False
+            fix: dict = {}
             if pending:
                 w = [x for x, _ in pending]
                 per = [q for _, q in pending]
@@ -190,10 +203,19 @@ class BatchedRepetendSearch:
                 self.counters.verified += len(w)
                 for i, (x, q) in enumerate(pending):
                     hints[(x, q)] = (int(st[i]), rows[i].copy())
-                    mispredicted |= int(st[i]) == _native.SAT
+                    if int(st[i]) == _native.SAT and (x not in fix or q < fix[x][0]):
+                        fix[x] = (q, rows[i].copy())
+            mispredicted = bool(fix)
+            unsafe = bool(set(fix) & res.retirers)
             if sync is not None:
                 mispredicted = sync.any(mispredicted)
+                unsafe = sync.any(unsafe)
             if not mispredicted:
+                return res
+            if not unsafe and self.repair:
+                for x, (q, row) in fix.items():
+                    res.first_sat[x] = (q, row)
+                self.counters.repaired += len(fix)
                 return res
             self.counters.redo += 1
         raise RuntimeError("speculation did not converge")

@@ -39,6 +39,13 @@ def main(name):
                                   for k, v in by_kind.items()}}))
     for row in sorted(tr, key=lambda r: -r[4])[:15]:
         print("top", row)
+    out = os.environ.get("TRACE_OUT")
+    if out:
+        Path(out).parent.mkdir(parents=True, exist_ok=True)
+        Path(out).write_text(json.dumps({"workload": name, "wall_s": wall,
+                                         "counters": {k: v for k, v in vars(eng.counters).items()
+                                                      if k != "trace"},
+                                         "trace": tr}))
 
 
 if __name__ == "__main__":

@@ -89,6 +89,11 @@ class OracleEngine:
         partial = stage_budget > 0 and (node_budget == 0 or stage_budget < node_budget)
         budget = stage_budget if partial else node_budget
         st = dict.fromkeys(STATS, 0)
+        if stage_budget < 0:  # filter-only stage; the stand-in has no filter
+            self.deferred = [w for w in self.deferred if w <= widx_limit]
+            st["deferred"] = len(self.deferred)
+            n, widx, rows = self._rows(max_sat)
+            return n, widx, rows, len(self.active), len(self.deferred), st
         redo = []
         for w in self.deferred:
             if w > widx_limit:

@@ -28,7 +28,7 @@ def _patch_decide(monkeypatch):
     monkeypatch.setattr(core, "decide", oracle_decide)
 
 
-def _run(name, comm=None, small_windows=False, speculate=True):
+def _run(name, comm=None, small_windows=False, speculate=True, repair=True, stage=8):
     import paper_2311_15269_b200.completion as C
     import paper_2311_15269_b200.engine as E
     from cpu_engine import OracleEngine
@@ -38,11 +38,12 @@ def _run(name, comm=None, small_windows=False, speculate=True):
     p = placement_from_dict(doc["placement"])
     eng = E.BatchedRepetendSearch(p, native=OracleEngine(p))
     eng.speculate = speculate
+    eng.repair = repair
     eng.resolve_stages = E.SPEC_STAGES if speculate else E.RESOLVE_STAGES
     if small_windows:  # many windows, many levels, many deferrals / speculations
         C.WINDOW_FIRST, C.WINDOW_GROWTH = 3, 2
         eng.small_budget = 2
-        eng.resolve_stages = ((0, 8),) if speculate else ((0, 8), (0, 0))
+        eng.resolve_stages = ((0, stage),) if speculate else ((0, 8), (0, 0))
     try:
         res = C.search(p, doc["mem_capacity"], max_nr=doc["max_nr"], engine=eng, comm=comm)
     finally:
@@ -85,16 +86,20 @@ def test_level_scan_and_replay_match_reference(monkeypatch, name, small, specula
     assert _summary(res) == _expected(doc)
 
 
-def test_speculation_mispredictions_are_repaired(monkeypatch):
+@pytest.mark.parametrize("repair,stage", [(True, 8), (True, -1), (False, 8)])
+def test_speculation_mispredictions_are_repaired(monkeypatch, repair, stage):
     """Tiny budgets make many probes pending; some verify SAT, forcing window
-    rescans — the result must still be exact."""
+    window repairs (or rescans when a mispredicted candidate had lowered a
+    retirement limit) — the result must still be exact."""
     _patch_decide(monkeypatch)
-    redo = 0
+    redo = repaired = 0
     for name in CASES:
-        doc, res = _run(name, small_windows=True, speculate=True)
+        doc, res = _run(name, small_windows=True, speculate=True, repair=repair, stage=stage)
         assert _summary(res) == _expected(doc)
         redo += res.report.engine["redo"]
-    assert redo > 0
+        repaired += res.report.engine["repaired"]
+    print("redo", redo, "repaired", repaired)
+    assert (repaired if repair else redo) > 0
 
 
 def _worker(rank, world, port, names, out_dir):
