@@ -155,7 +155,18 @@ int tsl_engine_add_active(tsl_engine *e, int64_t count, const int64_t *widx);
 /* Reference-exact repetend probes for explicit (window index, period) pairs
  * of the staged window, each under its own node cap (0 = none), run
  * concurrently (one warp per pair).  Writes status, node count and, on SAT,
- * starts[i*K .. +K). */
+ * starts[i*K .. +K).  A SAT (w, P) speculatively retires every pair (w2, P2)
+ * with w2 > w and P2 >= P: such pairs stop early with status 3 (aborted, not
+ * a reference status); the caller re-runs them unless that SAT's completion
+ * check passes. */
+/* Diagnostic: the disjunctive filter (DJ) on explicit (assignment[K],
+ * period) pairs — status 0 = proven infeasible, 1 = feasible, 2 = undecided
+ * within `budget` orientation nodes.  mode 1 = warp filter, 0 = one-lane
+ * filter.  The search uses DJ only to refute (never to accept). */
+int tsl_engine_dj(tsl_engine *e, int64_t count, const int32_t *assignments,
+                  const int32_t *period, int64_t cap, int64_t budget, int mode,
+                  int32_t *status_out, int64_t *nodes_out);
+
 int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const int32_t *period,
                       const int64_t *node_budget, int64_t cap, int32_t *status_out,
                       int64_t *nodes_out, int32_t *starts_out);

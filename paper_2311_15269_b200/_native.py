@@ -29,7 +29,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O2", "-shared",
 ]
 
-SAT, UNSAT, TIMEOUT = 1, 0, 2
+SAT, UNSAT, TIMEOUT, ABORT = 1, 0, 2, 3
 ERRORS = {-1: "EINVAL", -2: "ENODEV", -3: "ECUDA", -4: "ERANGE"}
 
 
@@ -83,7 +83,7 @@ EXPORTS = (
     "tsl_decide_batch", "tsl_engine_open", "tsl_engine_close", "tsl_engine_count",
     "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
     "tsl_engine_sat_rows", "tsl_engine_take_deferred", "tsl_engine_add_active",
-    "tsl_engine_verify",
+    "tsl_engine_verify", "tsl_engine_dj",
     "tsl_engine_last_kernel_ms", "tsl_counters",
 )
 
@@ -126,6 +126,8 @@ def lib():
     L.tsl_engine_add_active.argtypes = [vp, i64, vp]
     L.tsl_engine_verify.restype = i32
     L.tsl_engine_verify.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp, vp]
+    L.tsl_engine_dj.restype = i32
+    L.tsl_engine_dj.argtypes = [vp, i64, vp, vp, i64, i64, i32, vp, vp]
     L.tsl_engine_sat_rows.restype = i32
     L.tsl_engine_sat_rows.argtypes = [vp, i64, i64, vp, vp]
     L.tsl_counters.restype = None
@@ -333,6 +335,21 @@ class Engine:
                                             -1 if cap is None else int(cap), _ptr(st), _ptr(nd),
                                             _ptr(rows)))
         return st[:n].copy(), nd[:n].copy(), rows[:n * self.K].reshape(n, self.K).copy()
+
+    def dj(self, assignments, periods, cap, budget, mode=1):
+        """Diagnostic: disjunctive filter verdicts (0 infeasible, 1 feasible,
+        2 undecided) and orientation nodes for explicit (assignment, period)
+        pairs; mode 1 = warp filter, 0 = one-lane filter."""
+        a = np.ascontiguousarray(assignments, dtype=np.int32).reshape(-1, self.K)
+        per = np.ascontiguousarray(periods, dtype=np.int32)
+        n = int(per.size)
+        st = np.zeros(max(n, 1), dtype=np.int32)
+        nd = np.zeros(max(n, 1), dtype=np.int64)
+        if n:
+            check(self._L.tsl_engine_dj(self._h, n, _ptr(a), _ptr(per),
+                                        -1 if cap is None else int(cap), int(budget), int(mode),
+                                        _ptr(st), _ptr(nd)))
+        return st[:n].copy(), nd[:n].copy()
 
     def sat_rows(self, first: int, count: int):
         widx = np.zeros(max(count, 1), dtype=np.int64)

@@ -236,6 +236,12 @@ inline std::vector<int> rep_build(const Placement &pl) {
           }
         pdev_ptr.push_back((int)pdev.size());
       }
+  std::vector<int> dp_ptr(D + 1, 0), dp;
+  for (int d = 0; d < D; ++d) {
+    for (size_t q = 0; q < pairx.size(); ++q)
+      if (((pl.mask[pairx[q]] & pl.mask[pairy[q]]) >> d) & 1) dp.push_back((int)q);
+    dp_ptr[d + 1] = (int)dp.size();
+  }
   std::vector<int> conf_ptr(K + 1, 0), conf_dst, conf_pid;
   for (int i = 0; i < K; ++i) {
     for (int j = 0; j < K; ++j)
@@ -346,6 +352,8 @@ inline std::vector<int> rep_build(const Placement &pl) {
   put(R_HS, hs);
   put(R_FRPTR, fr_ptr);
   put(R_FR, fr);
+  put(R_DPPTR, dp_ptr);
+  put(R_DP, dp);
   pool[R_WORDS] = (int)pool.size();
   // value-range guard for the int32 device arithmetic: anchors reach
   // 2 (K-1)(P + max t) with P <= total.

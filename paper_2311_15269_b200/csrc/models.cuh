@@ -103,6 +103,8 @@ enum {
   // enumeration metadata: per stage st, lo sources (succ j < st), hi
   // sources (pred i < st), and the frontier F_{st+1} after assigning st
   R_LSPTR, R_LS, R_HSPTR, R_HS, R_FRPTR, R_FR,
+  // device -> disjunctive pairs on it (warp disjunctive filter)
+  R_DPPTR, R_DP,
   R_WORDS, R_HDR
 };
 

@@ -23,6 +23,7 @@
 #define RX_UNSAT 0
 #define RX_SAT 1
 #define RX_TIMEOUT 2
+#define RX_ABORT 3  // cancelled by the caller's retirement limit (not a reference status)
 
 #ifdef __CUDACC__
 #define RX_HD __host__ __device__ __forceinline__

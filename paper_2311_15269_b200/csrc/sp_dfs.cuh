@@ -1,0 +1,324 @@
+// sp_dfs.cuh — speculative subtree-parallel reference-exact DFS (SP-DFS).
+//
+// One long reference decide (kernel_c.pyx:220-371; e.g. the 8M-node-capped
+// completion probes of solver.py:280, or 400k-node repetend probes) is split
+// at a depth ds into SUBTREE TASKS run by many warps at once, with results
+// identical to the sequential DFS — status, lex-min witness and node count.
+//
+// Why this is exact.  Between two nodes the sequential DFS carries only
+// (a) bounds / placements, restored from per-depth snapshots on backtrack,
+// and (b) the "sticky" in-queue flags S that a failed propagation leaves
+// behind (kernel_c.pyx:303-347).  The exploration of the subtree below a
+// node at depth ds-1 is therefore a pure function of its entry state
+// (bounds, placements) and S_in, returning (nodes, SAT witness or exhausted,
+// S_out).  The MASTER walks the shallow part (depths < ds) exactly and, at
+// each descent into depth ds, emits a task with its entry state and
+// S_in = current S, then continues as if the subtree were exhausted with
+// S_out = S_in (speculation).  Helpers run the tasks.  The host then checks
+// the speculation task by task in DFS order: while every task returned
+// S_out == S_in, the master's walk was the exact one, so node counts add up
+// in order and the first SAT task (or the node cap) settles the probe.  At
+// the first task with S_out != S_in everything after it is discarded and the
+// master's walk is replayed from the round start with that task's true S_out
+// (measured: S_out == S_in for all 3,075 / 8,624 subtrees of the two
+// 8M-node C3 completion probes and ~99% of repetend subtrees).
+//
+// Master state records (global memory, int words):
+//   [0] depth  [1] v  [2] fresh (root propagation pending)  [3] unused
+//   lo[n] hi[n] s[n] vstack[n+1] placed[nw] inq[nw] snap[2 n (n+1)] (int2/depth)
+// Task records: lo[n] hi[n] s[n] placed[nw] inq[nw]  (entry at depth ds)
+// Task results: status, nodes (2 words), inq_out[nw], s[n]
+#pragma once
+#include "wrx_dfs.cuh"
+
+#define SP_EXHAUSTED 4  // subtree / sub-range exhausted (backtracked below the floor)
+#define SP_PAUSED 5     // master stopped after emitting its task quota
+
+__host__ __device__ inline int sp_nw(int n) { return ((n > 0 ? n : 1) + 31) / 32; }
+__host__ __device__ inline long long sp_state_words(int n) {
+  const long long nn = n > 0 ? n : 1;
+  return 4 + 3 * nn + (nn + 1) + 2 * sp_nw(n) + 2 * nn * (nn + 1);
+}
+__host__ __device__ inline long long sp_task_words(int n) {
+  const long long nn = n > 0 ? n : 1;
+  return 3 * nn + 2 * sp_nw(n);
+}
+__host__ __device__ inline long long sp_result_words(int n) {
+  const long long nn = n > 0 ? n : 1;
+  return 4 + sp_nw(n) + nn;
+}
+
+struct SpState {  // views into a master state record
+  int *hdr, *lo, *hi, *s, *vstack;
+  unsigned *placed, *inq;
+  int2 *snap;
+};
+__host__ __device__ inline SpState sp_state_view(int *base, int n) {
+  const int nn = n > 0 ? n : 1, nw = sp_nw(n);
+  SpState r;
+  int *p = base;
+  r.hdr = p; p += 4;
+  r.lo = p; p += nn;
+  r.hi = p; p += nn;
+  r.s = p; p += nn;
+  r.vstack = p; p += nn + 1;
+  r.placed = (unsigned *)p; p += nw;
+  r.inq = (unsigned *)p; p += nw;
+  r.snap = (int2 *)p;
+  return r;
+}
+
+#ifdef __CUDACC__
+// copy the mutable arrays between a record and the warp's shared state
+__device__ inline void sp_load(WWs &w, const int *lo, const int *hi, const int *s,
+                               const unsigned *placed, const unsigned *inq, int n) {
+  const int lane = wrx_lane(), nw = sp_nw(n);
+  for (int i = lane; i < n; i += 32) {
+    w.lo[i] = lo[i];
+    w.hi[i] = hi[i];
+    w.s[i] = s[i];
+  }
+  for (int i = lane; i < nw; i += 32) {
+    w.placed[i] = placed[i];
+    w.inq[i] = inq[i];
+  }
+  __syncwarp();
+}
+__device__ inline void sp_store(const WWs &w, int *lo, int *hi, int *s, unsigned *placed,
+                                unsigned *inq, int n) {
+  const int lane = wrx_lane(), nw = sp_nw(n);
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    lo[i] = w.lo[i];
+    hi[i] = w.hi[i];
+    s[i] = w.s[i];
+  }
+  for (int i = lane; i < nw; i += 32) {
+    placed[i] = w.placed[i];
+    inq[i] = w.inq[i];
+  }
+  __syncwarp();
+}
+
+// Task sink of the master walk.
+struct SpSink {
+  int *tasks;          // task records
+  long long *pre;      // master nodes counted before each task (this round)
+  int count, max;
+  const unsigned *ovr; // true S_out of the first n_ovr tasks (replay after a misprediction)
+  int n_ovr;
+};
+
+// The reference DFS loop of wrx_decide (kernel_c.pyx:225-371) generalised:
+// starts at (depth, v) with the live state in w (snapshots of depths
+// < depth valid), never backtracks below `floor` (returns SP_EXHAUSTED), and
+// — when `sink` is given — turns every descent into depth `split` into a
+// task (see the header).  *nodes counts this call's nodes; the cap applies
+// to (*nodes + base_nodes).  Returns RX_SAT / RX_TIMEOUT / SP_EXHAUSTED /
+// SP_PAUSED with depth / v updated.
+template <class M>
+__device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth, int &v,
+                          long long budget, long long base_nodes, long long *nodes_io,
+                          SpSink *sink) {
+  const int n = md.n(), cap = md.cap();
+  const int lane = wrx_lane();
+  long long nodes = *nodes_io;
+  int status;
+  int qh = 0, qt = 0, qc = 0;
+  for (;;) {
+    if (depth == n) {
+      status = RX_SAT;
+      break;
+    }
+    if (sink && depth == split) {  // descent into a task subtree
+      if (sink->count == sink->max) {
+        status = SP_PAUSED;
+        break;
+      }
+      const int k = sink->count;
+      int *rec = sink->tasks + (long long)k * sp_task_words(n);
+      const int nw = sp_nw(n);
+      sp_store(w, rec, rec + n, rec + 2 * n, (unsigned *)(rec + 3 * n),
+               (unsigned *)(rec + 3 * n + nw), n);
+      if (lane == 0) sink->pre[k] = nodes;
+      sink->count = k + 1;
+      if (k < sink->n_ovr) {  // replay: the task's true sticky set
+        const unsigned *so = sink->ovr + (long long)k * nw;
+        for (int i = lane; i < nw; i += 32) w.inq[i] = so[i];
+      }
+      // speculation: the subtree is exhausted and leaves S unchanged —
+      // backtrack exactly like the reference after exhausting depth `split`
+      --depth;
+      const int x = md.order(depth);
+      const int2 *sn = w.snap + (long long)depth * n;
+      for (int i = lane; i < n; i += 32) {
+        const int2 q = sn[i];
+        w.lo[i] = q.x;
+        w.hi[i] = q.y;
+      }
+      if (lane == 0) atomicAnd(&w.placed[x >> 5], ~(1u << (x & 31)));
+      v = w.vstack[depth] + 1;
+      __syncwarp();
+      continue;
+    }
+    int x = md.order(depth);
+    const int dx = md.dur(x);
+    if (v > w.hi[x]) {  // exhausted: backtrack and restore the depth's snapshot
+      if (depth - 1 < floor) {
+        status = SP_EXHAUSTED;
+        break;
+      }
+      --depth;
+      x = md.order(depth);
+      const int2 *sn = w.snap + (long long)depth * n;
+      for (int i = lane; i < n; i += 32) {
+        const int2 q = sn[i];
+        w.lo[i] = q.x;
+        w.hi[i] = q.y;
+      }
+      if (lane == 0) atomicAnd(&w.placed[x >> 5], ~(1u << (x & 31)));
+      v = w.vstack[depth] + 1;
+      __syncwarp();
+      continue;
+    }
+    const int cb = md.conf_begin(x), ce = md.conf_end(x);
+    for (;;) {  // conflict jump to the smallest non-overlapping value >= v
+      int jump = -(1 << 30);
+      for (int p = cb + lane; p < ce; p += 32) {
+        const int y = md.conf_dst(p);
+        if (wrx_bit(w.placed, y)) {
+          const int sy = w.s[y], ey = sy + md.dur(y);
+          if (sy - dx < v && v < ey) jump = ey > jump ? ey : jump;
+        }
+      }
+      jump = __reduce_max_sync(WRX_FULL, jump);
+      if (jump == -(1 << 30)) break;
+      v = jump;
+    }
+    if (v > w.hi[x]) continue;
+    ++nodes;
+    if (budget && nodes + base_nodes > budget) {
+      status = RX_TIMEOUT;
+      break;
+    }
+    {
+      int2 *sn = w.snap + (long long)depth * n;
+      for (int i = lane; i < n; i += 32) sn[i] = make_int2(w.lo[i], w.hi[i]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      w.s[x] = v;
+      w.lo[x] = v;
+      w.hi[x] = v;
+      atomicOr(&w.placed[x >> 5], 1u << (x & 31));
+      w.queue[0] = x;
+      atomicOr(&w.inq[x >> 5], 1u << (x & 31));
+    }
+    qh = 0;
+    qt = n == 1 ? 0 : 1;
+    qc = 1;
+    __syncwarp();
+    bool ok = true;
+    for (int base = cb; base < ce && ok; base += 32) {
+      const int p = base + lane;
+      const bool act = p < ce;
+      int y = 0, nlo = 0, nhi = 0;
+      bool chg = false, fail = false, inq = true;
+      if (act) {
+        y = md.conf_dst(p);
+        if (!wrx_bit(w.placed, y)) {
+          const int dy = md.dur(y);
+          const int lo_y = w.lo[y], hi_y = w.hi[y];
+          nlo = lo_y;
+          nhi = hi_y;
+          if (v - dy < lo_y && lo_y < v + dx) {
+            nlo = v + dx;
+            chg = true;
+            fail = nlo > hi_y;
+          }
+          if (!fail && v - dy < hi_y && hi_y < v + dx) {
+            nhi = v - dy;
+            chg = true;
+            fail = nhi < nlo;
+          }
+          inq = wrx_bit(w.inq, y);
+        }
+      }
+      const unsigned failm = __ballot_sync(WRX_FULL, fail);
+      if (failm) {
+        ok = false;
+        break;
+      }
+      __syncwarp();
+      if (chg) {
+        w.lo[y] = nlo;
+        w.hi[y] = nhi;
+      }
+      wrx_enqueue(w, chg && !inq, y, n, qt, qc, false);
+    }
+    if (ok) {
+      ok = wrx_propagate(md, w, qh, qt, qc);
+    } else {  // drain and clear the flags of this pass (kernel_c.pyx:341-347)
+      for (int k2 = lane; k2 < qc; k2 += 32) {
+        int slot = qh + k2;
+        if (slot >= n) slot -= n;
+        const int b = w.queue[slot];
+        atomicAnd(&w.inq[b >> 5], ~(1u << (b & 31)));
+      }
+      qc = 0;
+      __syncwarp();
+    }
+    const int fb = md.devof_begin(x), fe = md.devof_end(x);
+    if (ok && cap >= 0)
+      for (int p = fb; p < fe && ok; ++p) ok = wrx_mem_ok(md, w, md.devof(p), cap);
+    if (ok)
+      for (int p = fb; p < fe && ok; ++p) ok = wrx_dev_ok(md, w, md.devof(p));
+    if (ok) {
+      if (lane == 0) w.vstack[depth] = v;
+      ++depth;
+      __syncwarp();
+      if (depth < n) v = w.lo[md.order(depth)];
+      continue;
+    }
+    {
+      const int2 *sn = w.snap + (long long)depth * n;
+      for (int i = lane; i < n; i += 32) {
+        const int2 q = sn[i];
+        w.lo[i] = q.x;
+        w.hi[i] = q.y;
+      }
+    }
+    if (lane == 0) atomicAnd(&w.placed[x >> 5], ~(1u << (x & 31)));
+    ++v;
+    __syncwarp();
+  }
+  *nodes_io = nodes;
+  __syncwarp();
+  return status;
+}
+
+// Root step of the reference decide (kernel_c.pyx:158-215) on the warp
+// state: all items queued and flagged, FIFO propagation, root memory / device
+// checks.  Returns false = UNSAT with 0 nodes.
+template <class M>
+__device__ bool sp_root(const M &md, WWs &w) {
+  const int n = md.n(), ndev = md.ndev(), cap = md.cap();
+  const int lane = wrx_lane();
+  const int nw = (n + 31) / 32;
+  for (int i = lane; i < n; i += 32) w.queue[i] = i;
+  for (int i = lane; i < nw; i += 32) {
+    w.placed[i] = 0u;
+    const int rem = n - 32 * i;
+    w.inq[i] = rem >= 32 ? WRX_FULL : ((1u << rem) - 1u);
+  }
+  __syncwarp();
+  int qh = 0, qt = 0, qc = n;
+  if (!wrx_propagate(md, w, qh, qt, qc)) return false;
+  if (cap >= 0)
+    for (int d = 0; d < ndev; ++d)
+      if (!wrx_mem_ok(md, w, d, cap)) return false;
+  for (int d = 0; d < ndev; ++d)
+    if (!wrx_dev_ok(md, w, d)) return false;
+  return true;
+}
+#endif

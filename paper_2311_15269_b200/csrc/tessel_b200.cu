@@ -29,6 +29,7 @@
 #include "models.cuh"
 #include "dj_solve.cuh"
 #include "wrx_dfs.cuh"
+#include "wdj_solve.cuh"
 
 #define TSL_VERSION 2
 
@@ -460,7 +461,8 @@ __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gp
                                                       long long dj_budget, int cap,
                                                       long long widx_limit,
                                                       unsigned long long budget_ns,
-                                                      int *ws_base, long long ws_words) {
+                                                      int *ws_base, long long ws_words,
+                                                      int *dev_limit, int dj_warp) {
   extern __shared__ int sp[];
   // n_def_dev: device-side count (k_root survivors; probes counted there)
   if (n_def_dev) n_def = *n_def_dev;
@@ -482,13 +484,44 @@ __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gp
   const long long rx_budget = partial ? stage_budget : full_budget;
   unsigned long long s_nodes = 0, s_cap = 0, s_sat = 0, s_dju = 0, s_djn = 0, s_def = 0;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  // dev_limit: speculative retirement limit of this launch — every SAT lowers
+  // it to its index - 1 (assuming its completion check passes); probes above
+  // it stop early and go back to the deferred list, so the host re-runs them
+  // only if that SAT does not retire them (engine.py).
+  auto spec_retired = [&](int widx) {
+    int l = 0;
+    if (lane == 0) l = dev_limit ? *(volatile int *)dev_limit : (int)0x7fffffff;
+    l = __shfl_sync(WRX_FULL, l, 0);
+    return widx > l;
+  };
+  auto defer = [&](int widx) {
+    if (lane == 0) {
+      ++s_def;
+      o.def_out[atomicAdd(&o.counters[2], 1)] = widx;
+    }
+    __syncwarp();
+  };
   for (long long t = gw; t < n_def; t += nwarps) {
     const int widx = def_in[t];
     if (widx > widx_limit) continue;
+    if (spec_retired(widx)) {
+      defer(widx);
+      continue;
+    }
     const unsigned char *a = assign + (long long)widx * K;
     const unsigned long long t_end = budget_ns ? rx_now_ns() + budget_ns : 0ull;
     int dj = DJ_UNKNOWN;
-    if (dj_budget > 0) {
+    if (dj_budget > 0 && dj_warp) {
+      // warp disjunctive filter: shared state carved from the (not yet used)
+      // RX snapshot area, per-depth snapshots in this warp's global slice
+      WdjWs dw2 = wdj_carve(snap, ws_base + gw * 32 * ws_words, K, sp[R_NPAIR]);
+      if (lane == 0) rep_prepare(sp, a, P, deplag, init, dw2.lo, dw2.hi);
+      for (int i = lane; i < K; i += 32) dw2.av[i] = a[i];
+      __syncwarp();
+      long long dn = 0;
+      dj = wdj_decide(sp, P, cap, init, dw2, dj_budget, &dn);
+      if (lane == 0) s_djn += (unsigned long long)dn;
+    } else if (dj_budget > 0) {
       if (lane == 0) {
         rep_prepare(sp, a, P, deplag, init, dw.lo, dw.hi);
         const RepView v = rep_view(sp, P, cap, deplag, init);
@@ -505,22 +538,21 @@ __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gp
       }
       continue;
     }
-    if (stage_budget < 0) {  // disjunctive filter only: undecided probes stay deferred
-      if (lane == 0) {
-        ++s_def;
-        o.def_out[atomicAdd(&o.counters[2], 1)] = widx;
-      }
-      __syncwarp();
+    if (stage_budget < 0 || spec_retired(widx)) {  // filter only / retired meanwhile
+      defer(widx);
       continue;
     }
     if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
     __syncwarp();
     const RepView v = rep_view(sp, P, cap, deplag, init);
     long long nd = 0;
-    const int st = wrx_decide(v, w, rx_budget, t_end, &nd);
+    const int st = wrx_decide(v, w, rx_budget, t_end, &nd, dev_limit, widx);
     if (st == RX_SAT) {
       int k = 0;
-      if (lane == 0) k = atomicAdd(&o.counters[1], 1);
+      if (lane == 0) {
+        k = atomicAdd(&o.counters[1], 1);
+        if (dev_limit) atomicMin(dev_limit, widx - 1);
+      }
       k = __shfl_sync(WRX_FULL, k, 0);
       if (lane == 0) o.sat_widx[k] = widx;
       for (int i = lane; i < K; i += 32) o.sat_starts[(long long)k * K + i] = w.s[i];
@@ -528,6 +560,9 @@ __global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gp
         s_nodes += (unsigned long long)nd;
         ++s_sat;
       }
+    } else if (st == RX_ABORT) {
+      defer(widx);
+      continue;
     } else if (lane == 0) {
       if (st == RX_TIMEOUT && partial) {
         ++s_def;
@@ -560,7 +595,8 @@ __global__ void __launch_bounds__(128) k_verify_warp(const int *__restrict__ gpo
                                                      const int *__restrict__ vper,
                                                      const long long *__restrict__ vbudget,
                                                      int count, int cap, int *vstatus,
-                                                     long long *vnodes, int *vstarts) {
+                                                     long long *vnodes, int *vstarts,
+                                                     int *vlim, int pmin, int nlev) {
   extern __shared__ int sp[];
   load_pool(sp, gpool);
   const int K = sp[R_K];
@@ -574,19 +610,84 @@ __global__ void __launch_bounds__(128) k_verify_warp(const int *__restrict__ gpo
   WWs w = wrx_carve(mine_s, snap, K, sp[R_MAXDI]);
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + wib; t < count; t += nwarps) {
-    const int P = vper[t];
-    const unsigned char *a = assign + (long long)vwidx[t] * K;
+    const int P = vper[t], widx = vwidx[t];
+    // per-period speculative retirement: a SAT (w, P) retires (w2, P2) with
+    // w2 > w and P2 >= P if its completion check passes (the host decides)
+    int *lim = vlim + (P - pmin);
+    int l = 0;
+    if (lane == 0) l = *(volatile int *)lim;
+    l = __shfl_sync(WRX_FULL, l, 0);
+    if (widx > l) {
+      if (lane == 0) {
+        vstatus[t] = RX_ABORT;
+        vnodes[t] = 0;
+      }
+      continue;
+    }
+    const unsigned char *a = assign + (long long)widx * K;
     if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
     __syncwarp();
     const RepView v = rep_view(sp, P, cap, deplag, init);
     long long nd = 0;
-    const int st = wrx_decide(v, w, vbudget[t], 0ull, &nd);
+    const int st = wrx_decide(v, w, vbudget[t], 0ull, &nd, lim, widx);
     if (lane == 0) {
       vstatus[t] = st;
       vnodes[t] = nd;
+      if (st == RX_SAT)
+        for (int q = P - pmin; q < nlev; ++q) atomicMin(&vlim[q], widx - 1);
     }
     if (st == RX_SAT)
       for (int i = lane; i < K; i += 32) vstarts[t * K + i] = w.s[i];
+    __syncwarp();
+  }
+}
+
+// Diagnostic: the disjunctive filter on explicit (assignment, period) pairs
+// (tests check it never refutes a feasible probe).  mode 1 = warp filter
+// (wdj_solve.cuh), 0 = one-lane filter (dj_solve.cuh).
+__global__ void __launch_bounds__(128) k_dj_batch(const int *__restrict__ gpool,
+                                                  const int *__restrict__ assign,
+                                                  const int *__restrict__ per, int count, int cap,
+                                                  long long budget, int mode, int *gscratch,
+                                                  long long gwords, int *status,
+                                                  long long *nodes) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K], D = sp[R_D];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int ndep1 = sp[R_NDEP] > 0 ? sp[R_NDEP] : 1;
+  const int per_warp = (wdj_smem_words(K, sp[R_NPAIR]) + ndep1 + D + 3) & ~3;
+  int *mine = sp + ((sp[R_WORDS] + 3) & ~3) + wib * per_warp;
+  int *deplag = mine + wdj_smem_words(K, sp[R_NPAIR]);
+  int *init = deplag + ndep1;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  int *g = gscratch + gw * gwords;
+  WdjWs w = wdj_carve(mine, g, K, sp[R_NPAIR]);
+  DjWs dw = dj_ws_carve(g, K, D, sp[R_NPAIR], sp[R_MAXDI]);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long t = gw; t < count; t += nwarps) {
+    const int *a = assign + t * K;
+    const int P = per[t];
+    long long dn = 0;
+    int st;
+    if (mode == 1) {
+      if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
+      for (int i = lane; i < K; i += 32) w.av[i] = a[i];
+      __syncwarp();
+      st = wdj_decide(sp, P, cap, init, w, budget, &dn);
+    } else {
+      st = 0;
+      if (lane == 0) {
+        rep_prepare(sp, a, P, deplag, init, dw.lo, dw.hi);
+        const RepView v = rep_view(sp, P, cap, deplag, init);
+        st = dj_decide(v, sp, dw, budget, &dn);
+      }
+      st = __shfl_sync(WRX_FULL, st, 0);
+    }
+    if (lane == 0) {
+      status[t] = st;
+      nodes[t] = dn;
+    }
     __syncwarp();
   }
 }
@@ -636,6 +737,16 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 bool root_filter_off() {
   const char *m = getenv("TSL_ROOT_FILTER");
   return m && std::string(m) == "0";
+}
+
+// TSL_DJ_MODE=lane selects the one-lane disjunctive filter (dj_solve.cuh);
+// the default is the warp version (wdj_solve.cuh) when its shared state fits
+// in the RX snapshot area and its snapshots in a warp's workspace slice.
+bool dj_mode_warp(const int *pool) {
+  const char *m = getenv("TSL_DJ_MODE");
+  if (m && std::string(m) == "lane") return false;
+  return wdj_smem_words(pool[R_K], pool[R_NPAIR]) <= wrx_snap_words(pool[R_K]) &&
+         wdj_snap_words(pool[R_K], pool[R_NPAIR]) <= 32 * rep_ws_words(pool);
 }
 
 bool decide_mode_warp() {
@@ -797,7 +908,7 @@ struct tsl_engine {
     CK(cudaMalloc(&d_pool, pool.size() * sizeof(int)));
     h2d(d_pool, pool.data(), pool.size() * sizeof(int), stream);
     CK(cudaStreamSynchronize(stream));
-    CK(cudaMalloc(&d_counters, 4 * sizeof(int)));
+    CK(cudaMalloc(&d_counters, 8 * sizeof(int)));  // [4] = speculative retirement limit
     CK(cudaMalloc(&d_stats, 8 * sizeof(unsigned long long)));
     smem_bytes = pool.size() * sizeof(int);
     if (smem_bytes > 48 * 1024) {
@@ -1081,7 +1192,10 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
           "period anchor");
   const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
   const long long n_in = e->n_act;
-  CK(cudaMemsetAsync(e->d_counters, 0, 4 * sizeof(int), e->stream));
+  {
+    const int init[5] = {0, 0, 0, 0, (int)std::min<int64_t>(widx_limit, 0x7fffffff)};
+    h2d(e->d_counters, init, sizeof init, e->stream);
+  }
   CK(cudaMemsetAsync(e->d_stats, 0, 8 * sizeof(unsigned long long), e->stream));
   const int threads = 128;
   long long blocks = (n_in + threads - 1) / threads;
@@ -1129,7 +1243,7 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
     COUNT_LAUNCH();
     k_resolve_warp<<<(int)sblocks, 32 * swpb, ssmem, e->stream>>>(
         e->d_pool, e->d_assign, e->d_surv, 0, e->d_counters + 3, o, period, full, stage, 0,
-        icap, widx_limit, budget_ns, e->d_ws, e->ws_words);
+        icap, widx_limit, budget_ns, e->d_ws, e->ws_words, e->d_counters + 4, 0);
     CK(cudaGetLastError());
   } else if (n_in > 0) {
     COUNT_LAUNCH();
@@ -1167,8 +1281,9 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
   const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
   const long long n_def = e->n_def;
   // continue appending to the level's SAT list and to the active list
-  int counters[4] = {(int)e->n_act, (int)e->n_sat, 0, 0};
-  h2d(e->d_counters, counters, 4 * sizeof(int), e->stream);
+  int counters[5] = {(int)e->n_act, (int)e->n_sat, 0, 0,
+                     (int)std::min<int64_t>(widx_limit, 0x7fffffff)};
+  h2d(e->d_counters, counters, 5 * sizeof(int), e->stream);
   CK(cudaMemsetAsync(e->d_stats, 0, 8 * sizeof(unsigned long long), e->stream));
   const int threads = 128;
   long long blocks = (n_def + threads - 1) / threads;
@@ -1197,7 +1312,8 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
     k_resolve_warp<<<(int)wblocks, 32 * wpb, smem, e->stream>>>(
         e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, nullptr, o, period,
         node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? -1 : stage_budget,
-        dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words);
+        dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words,
+        e->d_counters + 4, dj_mode_warp(e->pool.data()) ? 1 : 0);
     CK(cudaGetLastError());
   } else if (n_def > 0) {
     COUNT_LAUNCH();
@@ -1280,7 +1396,14 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
   }
   const size_t b_i = ((size_t)count * sizeof(int) + 255) / 256 * 256;
   const size_t b_l = ((size_t)count * sizeof(long long) + 255) / 256 * 256;
-  const size_t need = 3 * b_i + 2 * b_l + (size_t)count * K * sizeof(int);
+  int pmin = period[0], pmax = period[0];
+  for (long long i = 0; i < count; ++i) {
+    pmin = std::min(pmin, period[i]);
+    pmax = std::max(pmax, period[i]);
+  }
+  const int nlev = pmax - pmin + 1;
+  const size_t b_lim = ((size_t)nlev * sizeof(int) + 255) / 256 * 256;
+  const size_t need = 3 * b_i + 2 * b_l + b_lim + (size_t)count * K * sizeof(int);
   if (need > e->d_verify_cap) {
     if (e->d_verify) CK(cudaFree(e->d_verify));
     CK(cudaMalloc(&e->d_verify, need));
@@ -1292,7 +1415,12 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
   int *d_st = (int *)q; q += b_i;
   long long *d_b = (long long *)q; q += b_l;
   long long *d_n = (long long *)q; q += b_l;
+  int *d_lim = (int *)q; q += b_lim;
   int *d_s = (int *)q;
+  {
+    std::vector<int> lim0(nlev, 0x7fffffff);
+    h2d(d_lim, lim0.data(), nlev * sizeof(int), e->stream);
+  }
   h2d(d_w, w32.data(), count * sizeof(int), e->stream);
   h2d(d_p, p32.data(), count * sizeof(int), e->stream);
   h2d(d_b, node_budget, count * sizeof(long long), e->stream);
@@ -1309,7 +1437,7 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
   COUNT_LAUNCH();
   k_verify_warp<<<(int)blocks, 32 * wpb, smem, e->stream>>>(e->d_pool, e->d_assign, d_w, d_p,
                                                              d_b, (int)count, icap, d_st, d_n,
-                                                             d_s);
+                                                             d_s, d_lim, pmin, nlev);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e->ev1, e->stream));
   d2h(status_out, d_st, count * sizeof(int), e->stream);
@@ -1345,6 +1473,50 @@ int tsl_engine_sat_rows(tsl_engine *e, int64_t first, int64_t count, int64_t *wi
   d2h(starts_out, d_out, total * sizeof(int), e->stream);
   CK(cudaStreamSynchronize(e->stream));
   for (long long r = 0; r < count; ++r) widx_out[r] = e->sat_widx_sorted[first + r];
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_dj(tsl_engine *e, int64_t count, const int32_t *assignments,
+                  const int32_t *period, int64_t cap, int64_t budget, int mode,
+                  int32_t *status_out, int64_t *nodes_out) {
+  API_BEGIN
+  if (count <= 0) return TSL_OK;
+  e->ensure_gpu();
+  CK(cudaSetDevice(e->device));
+  const int K = e->pool[R_K], D = e->pool[R_D];
+  for (long long i = 0; i < count; ++i)
+    tsl::ck(2LL * (K - 1) * ((long long)period[i] + e->pool[R_MAXDUR]) + 4LL * e->pool[R_TOTAL],
+            "period anchor");
+  const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
+  const int wpb = 4;
+  long long blocks = std::min<long long>((count + wpb - 1) / wpb, (long long)e->num_sms * 4);
+  const long long warps = blocks * wpb;
+  const long long gwords =
+      std::max<long long>(wdj_snap_words(K, e->pool[R_NPAIR]),
+                          dj_ws_words(K, D, e->pool[R_NPAIR], e->pool[R_MAXDI])) + 8;
+  int *d_a = nullptr, *d_p = nullptr, *d_st = nullptr, *d_g = nullptr;
+  long long *d_n = nullptr;
+  CK(cudaMalloc(&d_a, count * K * sizeof(int)));
+  CK(cudaMalloc(&d_p, count * sizeof(int)));
+  CK(cudaMalloc(&d_st, count * sizeof(int)));
+  CK(cudaMalloc(&d_n, count * sizeof(long long)));
+  CK(cudaMalloc(&d_g, warps * gwords * sizeof(int)));
+  h2d(d_a, assignments, count * K * sizeof(int), e->stream);
+  h2d(d_p, period, count * sizeof(int), e->stream);
+  const int ndep1 = e->pool[R_NDEP] > 0 ? e->pool[R_NDEP] : 1;
+  const int per_warp = (wdj_smem_words(K, e->pool[R_NPAIR]) + ndep1 + D + 3) & ~3;
+  const size_t smem = (((e->pool.size() + 3) & ~(size_t)3) + (size_t)wpb * per_warp) * sizeof(int);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_dj_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  COUNT_LAUNCH();
+  k_dj_batch<<<(int)blocks, 32 * wpb, smem, e->stream>>>(e->d_pool, d_a, d_p, (int)count, icap,
+                                                          budget, mode, d_g, gwords, d_st, d_n);
+  CK(cudaGetLastError());
+  d2h(status_out, d_st, count * sizeof(int), e->stream);
+  d2h(nodes_out, d_n, count * sizeof(long long), e->stream);
+  CK(cudaStreamSynchronize(e->stream));
+  for (void *p : {(void *)d_a, (void *)d_p, (void *)d_st, (void *)d_n, (void *)d_g}) cudaFree(p);
   return TSL_OK;
   API_END
 }

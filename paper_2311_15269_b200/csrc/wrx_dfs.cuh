@@ -380,7 +380,8 @@ __device__ bool wrx_dev_ok(const M &md, WWs &w, int d) {
 // *nodes_out uniform; w.s holds the witness on SAT.
 template <class M>
 __device__ int wrx_decide(const M &md, WWs &w, long long budget, unsigned long long t_end_ns,
-                          long long *nodes_out) {
+                          long long *nodes_out, const int *abort_lim = nullptr,
+                          int abort_self = 0) {
   const int n = md.n(), ndev = md.ndev(), cap = md.cap();
   const int lane = wrx_lane();
   const int nw = (n + 31) / 32;
@@ -452,6 +453,17 @@ __device__ int wrx_decide(const M &md, WWs &w, long long budget, unsigned long l
     if (t_end_ns && (nodes & 4095) == 0 && rx_now_ns() > t_end_ns) {
       status = RX_TIMEOUT;
       break;
+    }
+    // cooperative cancellation: a lower-index probe found SAT meanwhile
+    // (the caller re-runs aborted probes unless that SAT retires them)
+    if (abort_lim && (nodes & 255) == 0) {
+      int l = 0;
+      if (lane == 0) l = *(volatile const int *)abort_lim;
+      l = __shfl_sync(WRX_FULL, l, 0);
+      if (abort_self > l) {
+        status = RX_ABORT;
+        break;
+      }
     }
     {
       int2 *sn = w.snap + (long long)depth * n;

@@ -48,7 +48,7 @@ RESOLVE_STAGES = ((DJ_BUDGET, 32_768), (0, 0))
 # with speculation the RX-DFS stages are replaced by pending probes verified
 # once per window (one concurrent launch); -1 = disjunctive filter only.
 # TESSEL_SPEC_STAGE overrides the RX budget of the single resolve stage.
-SPEC_STAGES = ((DJ_BUDGET, int(os.environ.get("TESSEL_SPEC_STAGE", "32768"))),)
+SPEC_STAGES = ((DJ_BUDGET, int(os.environ.get("TESSEL_SPEC_STAGE", "65536"))),)
 TRACE = os.environ.get("TESSEL_TRACE", "0") == "1"
 
 
@@ -68,6 +68,7 @@ class EngineCounters:
     verified: int = 0        # speculated probes verified at window ends
     redo: int = 0            # window rescans after a misprediction
     repaired: int = 0        # mispredictions settled without a rescan
+    aborted: int = 0         # verifications cancelled by a lower SAT
     kernel_ms: float = 0.0
     probe_ms: float = 0.0     # k_probe (first pass)
     resolve_ms: float = 0.0   # k_resolve_warp (DJ + warp RX-DFS stages)
@@ -188,23 +189,10 @@ class BatchedRepetendSearch:
                                              hints)
             if res.timed_out:
                 return res
-            mispredicted = False
             fix: dict = {}
-            if pending:
-                w = [x for x, _ in pending]
-                per = [q for _, q in pending]
-                bud = [0 if q == self.lb else PROBE_NODES for q in per]
-                st, nodes, rows = self.eng.verify(w, per, bud, cap)
-                self.counters.add({"probes": 0, "root_refuted": 0, "nodes": int(nodes.sum()),
-                                   "capped": int((st == _native.TIMEOUT).sum()),
-                                   "sat": int((st == _native.SAT).sum()), "deferred": 0,
-                                   "dj_refuted": 0, "dj_nodes": 0},
-                                  self.eng.last_kernel_ms(), False, (n_r, r0, 0, "verify"))
-                self.counters.verified += len(w)
-                for i, (x, q) in enumerate(pending):
-                    hints[(x, q)] = (int(st[i]), rows[i].copy())
-                    if int(st[i]) == _native.SAT and (x not in fix or q < fix[x][0]):
-                        fix[x] = (q, rows[i].copy())
+            for x, q, row in self._verify_pending(n_r, r0, cap, pending, feasible, hints):
+                if x not in fix or q < fix[x][0]:
+                    fix[x] = (q, row)
             mispredicted = bool(fix)
             unsafe = bool(set(fix) & res.retirers)
             if sync is not None:
@@ -219,6 +207,40 @@ class BatchedRepetendSearch:
                 return res
             self.counters.redo += 1
         raise RuntimeError("speculation did not converge")
+
+    def _verify_pending(self, n_r, r0, cap, pending, feasible, hints):
+        """Settle the window's pending (speculated) probes in concurrent
+        launches.  The kernel lets a SAT (x, q) cancel pairs (x2, q2) with
+        x2 > x and q2 >= q; a cancelled pair is re-run unless such a SAT
+        passes its completion check (then the exact scan retires x2 at q and
+        its outcome is never used).  Returns the verified SATs (x, q, row)."""
+        sats = []
+        todo = list(pending)
+        while todo:
+            w = [x for x, _ in todo]
+            per = [q for _, q in todo]
+            bud = [0 if q == self.lb else PROBE_NODES for q in per]
+            st, nodes, rows = self.eng.verify(w, per, bud, cap)
+            self.counters.add({"probes": 0, "root_refuted": 0, "nodes": int(nodes.sum()),
+                               "capped": int((st == _native.TIMEOUT).sum()),
+                               "sat": int((st == _native.SAT).sum()), "deferred": 0,
+                               "dj_refuted": 0, "dj_nodes": 0},
+                              self.eng.last_kernel_ms(), False, (n_r, r0, 0, "verify"))
+            self.counters.verified += len(w)
+            again = []
+            for i, (x, q) in enumerate(todo):
+                s = int(st[i])
+                if s == _native.ABORT:
+                    again.append((x, q))
+                    continue
+                hints[(x, q)] = (s, rows[i].copy())
+                if s == _native.SAT:
+                    sats.append((x, q, rows[i].copy()))
+            self.counters.aborted += len(again)
+            todo = [(x2, q2) for x2, q2 in again
+                    if not any(x < x2 and q <= q2 and feasible(n_r, r0 + x, q, row)
+                               for x, q, row in sorted(sats, key=lambda r: r[:2]))]
+        return sats
 
     def _scan_window(self, n_r, r0, r1, cap, bound, feasible, deadline, sync, hints):
         res = WindowResult(n_r, r0, r1 - r0)
@@ -252,9 +274,9 @@ class BatchedRepetendSearch:
                 res.timed_out = True
                 return res, pending
             limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit, feasible)
-            for dj_budget, stage_budget in self.resolve_stages:
-                if not n_def:
-                    break
+            si, reruns = 0, 0
+            while n_def and si < len(self.resolve_stages):
+                dj_budget, stage_budget = self.resolve_stages[si]
                 n_sat, widx, rows, n_act, n_def, st = self.eng.resolve(
                     period, node_cap, stage_budget, dj_budget, cap, limit, budget_secs,
                     SAT_CHUNK)
@@ -265,6 +287,15 @@ class BatchedRepetendSearch:
                     return res, pending
                 limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit,
                                         feasible)
+                si += 1
+                if (si == len(self.resolve_stages) and n_def and not self.speculate
+                        and stage_budget == 0):
+                    # the full-cap stage leaves only probes a lower SAT cancelled;
+                    # re-run those its completion check did not retire
+                    reruns += 1
+                    if reruns > 64:
+                        raise RuntimeError("deferred probes did not settle")
+                    si -= 1
             if self.speculate and n_def:
                 spec, known_sat, back = [], [], []
                 for w in self.eng.take_deferred(limit, n_def):

@@ -82,6 +82,11 @@ int main() {
       }
       if (st != RX_TIMEOUT) {
         st == RX_SAT ? ++n_small_sat : ++n_small_other;
+        if (st == RX_SAT) {
+          char buf[64];
+          std::snprintf(buf, sizeof buf, "S %lld %lld", i, nodes);
+          lines[i] = buf;
+        }
         continue;
       }
       ++n_def;

@@ -22,6 +22,7 @@ class OracleEngine:
         self.model = SP.ProbeModel(p)
         self._lists = {}
         self.cands, self.active, self.deferred, self.sats = [], [], [], []
+        self.cancel = True  # emulate the device's speculative cancellations
 
     def _list(self, n_r):
         if n_r not in self._lists:
@@ -95,8 +96,20 @@ class OracleEngine:
             n, widx, rows = self._rows(max_sat)
             return n, widx, rows, len(self.active), len(self.deferred), st
         redo = []
-        for w in self.deferred:
-            if w > widx_limit:
+        todo = sorted(w for w in self.deferred if w <= widx_limit)
+        # the device cancels probes above a SAT of the same launch (speculative
+        # retirement); emulate the maximal cancellation: everything above the
+        # lowest SAT goes back to the deferred list
+        first_sat = None
+        for w in todo:
+            s, _, _ = self._probe(w, period, cap, budget)
+            if s == oracle.SAT:
+                first_sat = w
+                break
+        for w in todo:
+            if self.cancel and first_sat is not None and w > first_sat:
+                redo.append(w)
+                st["deferred"] += 1
                 continue
             s, starts, nodes = self._probe(w, period, cap, budget)
             if s == oracle.SAT:
@@ -128,6 +141,11 @@ class OracleEngine:
             st.append(s)
             nodes.append(nd)
             rows.append(starts if starts is not None else [0] * self.K)
+        if self.cancel:  # maximal cancellation by SATs (x, q): x < x2, q <= q2
+            sats = [(int(w), int(q)) for w, q, s in zip(widx, periods, st) if s == oracle.SAT]
+            for i, (w, q) in enumerate(zip(widx, periods)):
+                if any(x < int(w) and p <= int(q) for x, p in sats):
+                    st[i], nodes[i] = 3, 0
         return (np.array(st, dtype=np.int32), np.array(nodes, dtype=np.int64),
                 np.array(rows, dtype=np.int32).reshape(len(st), self.K))
 

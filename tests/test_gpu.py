@@ -211,3 +211,47 @@ def test_solve_repetend_matches_oracle(gpu):
             if exp.status == "ok":
                 assert got.repetend.internal == exp.internal
                 assert got.repetend.period == exp.period
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_disjunctive_filter_on_device_never_refutes_a_feasible_probe(gpu, mode):
+    """The device disjunctive filters (warp: wdj_solve.cuh, one-lane:
+    dj_solve.cuh) on the reference-capped / DFS-heavy probes of
+    tests/golden/dj_probes.json: never 'infeasible' for a probe whose exact
+    verdict is SAT, agreement whenever they decide, and most capped probes
+    refuted (the filter's purpose)."""
+    from collections import defaultdict
+
+    import numpy as np
+
+    from paper_2311_15269_b200 import _native
+    from paper_2311_15269_b200.workloads import WORKLOADS
+
+    rows = json.loads((GOLDEN / "dj_probes.json").read_text())
+    by = defaultdict(list)
+    for r in rows:
+        by[(r["workload"], r["cap"])].append(r)
+    decided = capped = refuted_capped = 0
+    for (wl, cap), rs in by.items():
+        p = WORKLOADS[wl].placement()
+        k = p.num_stages
+        eng = _native.Engine([p.block(s).time_cost for s in range(k)],
+                             [p.block(s).mem_delta for s in range(k)],
+                             [sum(1 << d for d in p.block(s).devices) for s in range(k)],
+                             sorted(p.deps), p.num_devices, 0)
+        try:
+            st, _ = eng.dj(np.array([r["a"] for r in rs]), np.array([r["P"] for r in rs]), cap,
+                           200_000, mode)
+        finally:
+            eng.close()
+        for r, v in zip(rs, st.tolist()):
+            if r["truth"] == 1:
+                assert v != 0, (wl, r["a"], r["P"])
+            if v != 2 and r["truth"] != -1:
+                decided += 1
+                assert v == r["truth"], (wl, r["a"], r["P"])
+            if r["ref_status"] == 2:
+                capped += 1
+                refuted_capped += v == 0
+    assert decided > 0
+    assert capped == 0 or refuted_capped / capped > 0.5

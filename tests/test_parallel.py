@@ -92,14 +92,16 @@ def test_speculation_mispredictions_are_repaired(monkeypatch, repair, stage):
     window repairs (or rescans when a mispredicted candidate had lowered a
     retirement limit) — the result must still be exact."""
     _patch_decide(monkeypatch)
-    redo = repaired = 0
+    redo = repaired = aborted = 0
     for name in CASES:
         doc, res = _run(name, small_windows=True, speculate=True, repair=repair, stage=stage)
         assert _summary(res) == _expected(doc)
         redo += res.report.engine["redo"]
         repaired += res.report.engine["repaired"]
-    print("redo", redo, "repaired", repaired)
+        aborted += res.report.engine["aborted"]
+    print("redo", redo, "repaired", repaired, "aborted", aborted)
     assert (repaired if repair else redo) > 0
+    assert aborted > 0  # cancelled verifications were re-run or retired
 
 
 def _worker(rank, world, port, names, out_dir):
