@@ -20,8 +20,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_PATH = PKG / "libtessel_b200.so"
 SOURCES = [PKG / "csrc" / "tessel_b200.cu"]
-HEADERS = [PKG / "csrc" / "rx_dfs.cuh", PKG / "csrc" / "models.cuh",
-           PKG / "csrc" / "host_build.hpp", ROOT / "include" / "tessel_b200.h"]
+HEADERS = sorted((PKG / "csrc").glob("*.cuh")) + sorted((PKG / "csrc").glob("*.inc")) + [
+    PKG / "csrc" / "host_build.hpp", ROOT / "include" / "tessel_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

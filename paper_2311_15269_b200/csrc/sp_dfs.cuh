@@ -26,7 +26,8 @@
 // Master state records (global memory, int words):
 //   [0] depth  [1] v  [2] fresh (root propagation pending)  [3] unused
 //   lo[n] hi[n] s[n] vstack[n+1] placed[nw] inq[nw] snap[2 n (n+1)] (int2/depth)
-// Task records: lo[n] hi[n] s[n] placed[nw] inq[nw]  (entry at depth ds)
+// Task records: lo[n] hi[n] s[n] placed[nw] inq[nw] v depth  (the rest of
+//   depth `depth` from value v, and everything below it)
 // Task results: status, nodes (2 words), inq_out[nw], s[n]
 #pragma once
 #include "wrx_dfs.cuh"
@@ -35,13 +36,19 @@
 #define SP_PAUSED 5     // master stopped after emitting its task quota
 
 __host__ __device__ inline int sp_nw(int n) { return ((n > 0 ? n : 1) + 31) / 32; }
+// words before the snapshot area, rounded up so the int2 snapshots are aligned
+__host__ __device__ inline long long sp_state_head(int n) {
+  const long long nn = n > 0 ? n : 1;
+  return (4 + 3 * nn + (nn + 1) + 2 * sp_nw(n) + 3) / 4 * 4;
+}
 __host__ __device__ inline long long sp_state_words(int n) {
   const long long nn = n > 0 ? n : 1;
-  return 4 + 3 * nn + (nn + 1) + 2 * sp_nw(n) + 2 * nn * (nn + 1);
+  return sp_state_head(n) + 2 * nn * (nn + 1);
 }
+// task record: lo[n] hi[n] s[n] placed[nw] inq[nw] v depth
 __host__ __device__ inline long long sp_task_words(int n) {
   const long long nn = n > 0 ? n : 1;
-  return 3 * nn + 2 * sp_nw(n);
+  return 3 * nn + 2 * sp_nw(n) + 2;
 }
 __host__ __device__ inline long long sp_result_words(int n) {
   const long long nn = n > 0 ? n : 1;
@@ -63,8 +70,8 @@ __host__ __device__ inline SpState sp_state_view(int *base, int n) {
   r.s = p; p += nn;
   r.vstack = p; p += nn + 1;
   r.placed = (unsigned *)p; p += nw;
-  r.inq = (unsigned *)p; p += nw;
-  r.snap = (int2 *)p;
+  r.inq = (unsigned *)p;
+  r.snap = (int2 *)(base + sp_state_head(n));
   return r;
 }
 
@@ -103,10 +110,17 @@ __device__ inline void sp_store(const WWs &w, int *lo, int *hi, int *s, unsigned
 // Task sink of the master walk.
 struct SpSink {
   int *tasks;          // task records
-  long long *pre;      // master nodes counted before each task (this round)
+  long long *pre;      // master nodes counted before each task (this walk)
   int count, max;
   const unsigned *ovr; // true S_out of the first n_ovr tasks (replay after a misprediction)
   int n_ovr;
+  // replay checkpoints: the full master state right before emitting task
+  // k = j * ck_every (state record j of `ck`, its round-relative node count
+  // in ck_nodes[j]), written for j >= ck_have
+  int *ck;
+  long long *ck_nodes;
+  int ck_every, ck_have;
+  long long ck_base;
 };
 
 // The reference DFS loop of wrx_decide (kernel_c.pyx:225-371) generalised:
@@ -119,7 +133,7 @@ struct SpSink {
 template <class M>
 __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth, int &v,
                           long long budget, long long base_nodes, long long *nodes_io,
-                          SpSink *sink) {
+                          SpSink *sink, long long pause_nodes = 0, int *hist = nullptr) {
   const int n = md.n(), cap = md.cap();
   const int lane = wrx_lane();
   long long nodes = *nodes_io;
@@ -130,17 +144,45 @@ __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth,
       status = RX_SAT;
       break;
     }
-    if (sink && depth == split) {  // descent into a task subtree
+    if (pause_nodes && nodes >= pause_nodes) {  // a consistent resume point
+      status = SP_PAUSED;
+      break;
+    }
+    if (sink && depth >= split) {  // the rest of this depth becomes a task
+      // (at a descent into `split` that is a whole subtree; a master standing
+      // deeper — after a resume or a split change — climbs back emitting
+      // the rest of every depth on its way, deepest first = DFS order)
       if (sink->count == sink->max) {
         status = SP_PAUSED;
         break;
       }
       const int k = sink->count;
-      int *rec = sink->tasks + (long long)k * sp_task_words(n);
       const int nw = sp_nw(n);
+      if (sink->ck && k % sink->ck_every == 0 && k / sink->ck_every >= sink->ck_have) {
+        const int j = k / sink->ck_every;
+        SpState c = sp_state_view(sink->ck + (long long)j * sp_state_words(n), n);
+        sp_store(w, c.lo, c.hi, c.s, c.placed, c.inq, n);
+        for (int i = lane; i <= n; i += 32) c.vstack[i] = w.vstack[i];
+        for (long long i = lane; i < (long long)depth * n; i += 32) c.snap[i] = w.snap[i];
+        if (lane == 0) {
+          c.hdr[0] = depth;
+          c.hdr[1] = v;
+          c.hdr[2] = 0;
+          sink->ck_nodes[j] = sink->ck_base + nodes;
+        }
+        __syncwarp();
+      }
+      int *rec = sink->tasks + (long long)k * sp_task_words(n);
       sp_store(w, rec, rec + n, rec + 2 * n, (unsigned *)(rec + 3 * n),
                (unsigned *)(rec + 3 * n + nw), n);
-      if (lane == 0) sink->pre[k] = nodes;
+      // the task is the rest of depth `split` from value v (a fresh descent
+      // has v = lo[order(split)]; after a resume or a split change the master
+      // can also stand inside depth `split`) and everything below it
+      if (lane == 0) {
+        sink->pre[k] = nodes;
+        rec[3 * n + 2 * nw] = v;
+        rec[3 * n + 2 * nw + 1] = depth;
+      }
       sink->count = k + 1;
       if (k < sink->n_ovr) {  // replay: the task's true sticky set
         const unsigned *so = sink->ovr + (long long)k * nw;
@@ -201,6 +243,7 @@ __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth,
       status = RX_TIMEOUT;
       break;
     }
+    if (hist && lane == 0) ++hist[depth];
     {
       int2 *sn = w.snap + (long long)depth * n;
       for (int i = lane; i < n; i += 32) sn[i] = make_int2(w.lo[i], w.hi[i]);

@@ -19,6 +19,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <ctime>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -30,6 +32,7 @@
 #include "dj_solve.cuh"
 #include "wrx_dfs.cuh"
 #include "wdj_solve.cuh"
+#include "sp_dfs.cuh"
 
 #define TSL_VERSION 2
 
@@ -700,6 +703,98 @@ __global__ void k_gather_rows(const int *__restrict__ rows, const int *__restric
   out[t] = rows[(long long)pos[r] * K + i];
 }
 
+// ------------------------------------------------------------------ SP-DFS
+// Speculative subtree-parallel decide for one long general problem
+// (sp_dfs.cuh): the master walk (one warp) and the subtree tasks (one warp
+// each).  Shared per warp: the WRX state; snapshots in global memory.
+__global__ void __launch_bounds__(32) k_sp_master(const int *__restrict__ pool, int *state,
+                                                  int floor, int split, long long budget,
+                                                  long long base_nodes, long long pause_nodes,
+                                                  int *tasks, long long *pre, int max_tasks,
+                                                  const unsigned *ovr, int n_ovr, int *hist,
+                                                  long long *out, int k0, int *ck,
+                                                  long long *ck_nodes, int ck_every, int ck_have,
+                                                  long long ck_base) {
+  extern __shared__ int sm[];
+  const int lane = threadIdx.x & 31;
+  const GenView g = gen_view(pool);
+  const int n = g.n_;
+  SpState st = sp_state_view(state, n);
+  WWs w = wrx_carve(sm, (int *)st.snap, n, pool[G_MAXDI]);
+  int depth = 0, v = 0, status = -1;
+  long long nodes = 0;
+  if (st.hdr[2]) {  // fresh: the reference root step
+    for (int k = lane; k < n; k += 32) {
+      w.lo[k] = g.lo_[k];
+      w.hi[k] = g.hi_[k];
+    }
+    __syncwarp();
+    if (!sp_root(g, w)) status = RX_UNSAT;
+    else if (n == 0) status = RX_SAT;
+    else v = w.lo[g.order(0)];
+  } else {
+    sp_load(w, st.lo, st.hi, st.s, st.placed, st.inq, n);
+    for (int k = lane; k <= n; k += 32) w.vstack[k] = st.vstack[k];
+    depth = st.hdr[0];
+    v = st.hdr[1];
+    __syncwarp();
+  }
+  SpSink sink{tasks, pre, k0, max_tasks, ovr, n_ovr, ck, ck_nodes, ck_every, ck_have, ck_base};
+  if (status < 0)
+    status = sp_explore(g, w, floor, split, depth, v, budget, base_nodes, &nodes,
+                        split <= n ? &sink : nullptr, pause_nodes, hist);
+  sp_store(w, st.lo, st.hi, st.s, st.placed, st.inq, n);
+  for (int k = lane; k <= n; k += 32) st.vstack[k] = w.vstack[k];
+  if (lane == 0) {
+    st.hdr[0] = depth;
+    st.hdr[1] = v;
+    st.hdr[2] = 0;
+    out[0] = status;
+    out[1] = sink.count;
+    out[2] = nodes;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
+                                                  const int *__restrict__ tasks, int first,
+                                                  int count, int split, long long budget,
+                                                  int *snaps, int *results, int *info) {
+  extern __shared__ int sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const GenView g = gen_view(pool);
+  const int n = g.n_, nw = sp_nw(n);
+  const int per_warp = (wrx_state_words(n, pool[G_MAXDI]) + 3) & ~3;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  WWs w = wrx_carve(sm + wib * per_warp, snaps + gw * 2LL * n * (n + 1), n, pool[G_MAXDI]);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long t = first + gw; t < first + count; t += nwarps) {
+    const int *rec = tasks + t * sp_task_words(n);
+    sp_load(w, rec, rec + n, rec + 2 * n, (const unsigned *)(rec + 3 * n),
+            (const unsigned *)(rec + 3 * n + nw), n);
+    int v = rec[3 * n + 2 * nw], depth = rec[3 * n + 2 * nw + 1];
+    long long nodes = 0;
+    const int st = sp_explore(g, w, depth, n + 1, depth, v, budget, 0, &nodes, nullptr);
+    int *res = results + t * sp_result_words(n);
+    bool moved = false;  // S_out != S_in: the master's speculation failed here
+    for (int i = lane; i < nw; i += 32) moved |= w.inq[i] != (unsigned)rec[3 * n + nw + i];
+    moved = __any_sync(WRX_FULL, moved);
+    if (lane == 0) {
+      res[0] = st;
+      res[1] = (int)(nodes & 0xffffffffLL);
+      res[2] = (int)(nodes >> 32);
+      res[3] = moved ? 1 : 0;
+      info[4 * t + 0] = st;
+      info[4 * t + 1] = res[1];
+      info[4 * t + 2] = res[2];
+      info[4 * t + 3] = res[3];
+    }
+    for (int i = lane; i < nw; i += 32) res[4 + i] = (int)w.inq[i];
+    if (st == RX_SAT)
+      for (int i = lane; i < n; i += 32) res[4 + nw + i] = w.s[i];
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------------ decide API
 
 namespace {
@@ -730,6 +825,8 @@ DecideCtx &decide_ctx() {
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+#include "sp_host.inc"
+
 // TSL_DFS_MODE=thread selects the one-thread-per-probe DFS kernels (kept for
 // cross-validation); the default is the warp-cooperative DFS.
 // TSL_ROOT_FILTER=0 disables k_root (every probe runs k_probe's thread DFS;
@@ -755,7 +852,7 @@ bool decide_mode_warp() {
 }
 
 void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, int32_t *status,
-                      int64_t *nodes, int64_t *starts, int stride) {
+                      int64_t *nodes, int64_t *starts, int stride, bool allow_sp) {
   require_device();
   if (count <= 0) return;
   std::vector<int> pools;
@@ -779,6 +876,13 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
     budgets[i] = p.node_budget < 0 ? 0 : p.node_budget;
     max_n = std::max(max_n, p.n);
   }
+  // long problems: a first pass of SP_FIRST nodes here; the ones still open
+  // then run subtree-parallel (sp_solve) with their real cap
+  const bool sp = allow_sp && warp_mode && sp_enabled();
+  std::vector<long long> real_budget(budgets);
+  if (sp)
+    for (int i = 0; i < count; ++i)
+      if (budgets[i] == 0 || budgets[i] >= SP_MIN_BUDGET) budgets[i] = SP_FIRST;
   if (stride < max_n) throw tsl::Error(TSL_EINVAL, "starts stride smaller than a problem size");
   DecideCtx &ctx = decide_ctx();
   std::lock_guard<std::mutex> lock(ctx.mu);
@@ -835,9 +939,42 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
   d2h(h_nd.data(), d_nd, count * sizeof(long long), s);
   d2h(h_starts.data(), d_starts, (size_t)count * stride * sizeof(int), s);
   CK(cudaStreamSynchronize(s));
+  // many long problems: they run concurrently (one warp each) at their real
+  // cap; a few: one at a time, each subtree-parallel over the whole GPU
+  std::vector<int> longs;
+  for (int i = 0; i < count; ++i)
+    if (sp && h_st[i] == RX_TIMEOUT && budgets[i] != real_budget[i]) longs.push_back(i);
+  if ((int)longs.size() > SP_BATCH_MAX) {
+    std::vector<tsl_problem> sub;
+    for (int i : longs) sub.push_back(probs[i]);
+    std::vector<int32_t> st2(longs.size());
+    std::vector<int64_t> nd2(longs.size()), s2((size_t)longs.size() * stride);
+    run_decide_batch((int)longs.size(), sub.data(), budget_secs, st2.data(), nd2.data(),
+                     s2.data(), stride, /*allow_sp=*/false);
+    for (size_t k = 0; k < longs.size(); ++k) {
+      const int i = longs[k];
+      h_st[i] = st2[k];
+      h_nd[i] = nd2[k];
+      for (int j = 0; j < probs[i].n; ++j)
+        h_starts[(size_t)i * stride + j] = (int)s2[k * stride + j];
+      budgets[i] = real_budget[i];
+    }
+  }
   for (int i = 0; i < count; ++i) {
     status[i] = h_st[i];
     nodes[i] = h_nd[i];
+    if (sp && h_st[i] == RX_TIMEOUT && budgets[i] != real_budget[i]) {
+      std::vector<int> one(pools.begin() + pool_off[i],
+                           pools.begin() + pool_off[i] + pools[pool_off[i] + G_WORDS]);
+      std::vector<int> sv(std::max(probs[i].n, 1));
+      long long nd = 0;
+      const int st = sp_solve(one, real_budget[i], budget_secs, s, &nd, sv.data());
+      status[i] = st;
+      nodes[i] = nd;
+      if (starts && st == RX_SAT)
+        for (int k = 0; k < probs[i].n; ++k) starts[(size_t)i * stride + k] = sv[k];
+      continue;
+    }
     if (starts && h_st[i] == RX_SAT)
       for (int k = 0; k < probs[i].n; ++k)
         starts[(size_t)i * stride + k] = h_starts[(size_t)i * stride + k];
@@ -1027,7 +1164,7 @@ int tsl_decide(int n, const int64_t *dur, const uint64_t *devmask, const int64_t
   p.node_budget = node_budget;
   int32_t st = 0;
   int64_t nd = 0;
-  run_decide_batch(1, &p, budget_secs, &st, &nd, out_starts, std::max(n, 1));
+  run_decide_batch(1, &p, budget_secs, &st, &nd, out_starts, std::max(n, 1), true);
   if (out_nodes) *out_nodes = nd;
   return st;
   API_END
@@ -1037,7 +1174,7 @@ int tsl_decide_batch(int count, const tsl_problem *probs, double budget_secs, in
                      int64_t *nodes, int64_t *starts, int stride) {
   API_BEGIN
   if (count < 0) throw tsl::Error(TSL_EINVAL, "negative problem count");
-  run_decide_batch(count, probs, budget_secs, status, nodes, starts, stride);
+  run_decide_batch(count, probs, budget_secs, status, nodes, starts, stride, true);
   return TSL_OK;
   API_END
 }

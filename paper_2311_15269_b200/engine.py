@@ -40,6 +40,12 @@ WINDOW_GROWTH = 4
 WINDOW_MAX = 1 << 21
 SAT_CHUNK = 256
 SMALL_BUDGET = 64     # first-pass RX-DFS nodes per probe (thread per probe) before deferral
+# node cap of the concurrent verify pass; longer probes run one at a time
+# through the decide path (subtree-parallel for unlimited / >= 1M caps).
+# Default: off — capped repetend probes change their sticky sets too often
+# for the speculation to pay (tests/native/sp_sim.cpp model), so they stay
+# one warp each, all concurrently.
+VERIFY_FIRST = int(os.environ.get("TESSEL_VERIFY_FIRST", str(1 << 40)))
 DJ_BUDGET = 200_000   # disjunctive-refutation nodes per deferred probe
 # escalation of deferred probes: (DJ budget, RX-DFS stage budget; 0 = the
 # reference cap).  The retirement limit is re-applied between stages, so a
@@ -69,6 +75,7 @@ class EngineCounters:
     redo: int = 0            # window rescans after a misprediction
     repaired: int = 0        # mispredictions settled without a rescan
     aborted: int = 0         # verifications cancelled by a lower SAT
+    sp_probes: int = 0       # long probes settled by the subtree-parallel decide
     kernel_ms: float = 0.0
     probe_ms: float = 0.0     # k_probe (first pass)
     resolve_ms: float = 0.0   # k_resolve_warp (DJ + warp RX-DFS stages)
@@ -124,6 +131,7 @@ class BatchedRepetendSearch:
         self.speculate = os.environ.get("TESSEL_SPECULATE", "1") == "1"
         self.resolve_stages = SPEC_STAGES if self.speculate else RESOLVE_STAGES
         self.repair = os.environ.get("TESSEL_REPAIR", "1") == "1"
+        self._last_ms = 0.0
 
     def _scan_sats(self, res, n_r, r0, period, n_sat, widx, rows, limit, feasible, extra=()):
         """Walk the level's SAT rows (device list, already sorted, merged with
@@ -216,31 +224,77 @@ class BatchedRepetendSearch:
         its outcome is never used).  Returns the verified SATs (x, q, row)."""
         sats = []
         todo = list(pending)
+
+        def justified(x2, q2):
+            return any(x < x2 and q <= q2 and feasible(n_r, r0 + x, q, row)
+                       for x, q, row in sorted(sats, key=lambda r: r[:2]))
+
         while todo:
             w = [x for x, _ in todo]
             per = [q for _, q in todo]
             bud = [0 if q == self.lb else PROBE_NODES for q in per]
-            st, nodes, rows = self.eng.verify(w, per, bud, cap)
+            # one concurrent launch settles the probes that end within
+            # VERIFY_FIRST nodes; longer ones run one at a time through the
+            # subtree-parallel decide (sp_dfs.cuh) below
+            run_bud = [VERIFY_FIRST if (b == 0 or b > VERIFY_FIRST) else b for b in bud]
+            st, nodes, rows = self.eng.verify(w, per, run_bud, cap)
             self.counters.add({"probes": 0, "root_refuted": 0, "nodes": int(nodes.sum()),
                                "capped": int((st == _native.TIMEOUT).sum()),
                                "sat": int((st == _native.SAT).sum()), "deferred": 0,
                                "dj_refuted": 0, "dj_nodes": 0},
                               self.eng.last_kernel_ms(), False, (n_r, r0, 0, "verify"))
             self.counters.verified += len(w)
-            again = []
+            again, long = [], []
             for i, (x, q) in enumerate(todo):
                 s = int(st[i])
                 if s == _native.ABORT:
                     again.append((x, q))
                     continue
+                if s == _native.TIMEOUT and run_bud[i] != bud[i]:
+                    long.append((x, q, bud[i]))
+                    continue
                 hints[(x, q)] = (s, rows[i].copy())
                 if s == _native.SAT:
                     sats.append((x, q, rows[i].copy()))
+            for x, q, b in sorted(long):
+                if justified(x, q):
+                    continue  # retired at q by a lower completion-feasible SAT
+                s, row, nd = self._long_probe(n_r, r0 + x, q, cap, b)
+                self.counters.add({"probes": 0, "root_refuted": 0, "nodes": nd,
+                                   "capped": int(s == _native.TIMEOUT),
+                                   "sat": int(s == _native.SAT), "deferred": 0,
+                                   "dj_refuted": 0, "dj_nodes": 0},
+                                  self._last_ms, False, (n_r, r0, q, "verify-sp"))
+                self.counters.sp_probes += 1
+                hints[(x, q)] = (s, row)
+                if s == _native.SAT:
+                    sats.append((x, q, row))
             self.counters.aborted += len(again)
-            todo = [(x2, q2) for x2, q2 in again
-                    if not any(x < x2 and q <= q2 and feasible(n_r, r0 + x, q, row)
-                               for x, q, row in sorted(sats, key=lambda r: r[:2]))]
+            todo = [(x2, q2) for x2, q2 in again if not justified(x2, q2)]
         return sats
+
+    def _long_probe(self, n_r, rank, period, cap, budget):
+        """One repetend probe as a general reference decide (the lowering of
+        repetend.py:108-190 in repetend._CandidateModel), which the decide
+        path runs subtree-parallel when it is long."""
+        from . import _core
+        from .repetend import _model_for, entry_memory
+
+        a = self.eng.unrank(n_r, rank)
+        m = _model_for(self.p)
+        m.set_assignment(a)
+        anchor = (m.k - 1) * (period + m.max_dur)
+        lo = [0] * m.k
+        hi = [2 * anchor] * m.k
+        if m.k:
+            lo[0] = hi[0] = anchor
+        t0 = time.perf_counter()
+        status, starts, nodes = _core.decide(
+            m.k, m.dur, m.mask, m.mem, m.edges(period), m.order, lo, hi, self.p.num_devices,
+            list(entry_memory(self.p, a)), -1 if cap is None else cap, budget, 0.0)
+        self._last_ms = (time.perf_counter() - t0) * 1e3
+        row = np.array(starts if starts is not None else [0] * m.k, dtype=np.int32)
+        return int(status), row, int(nodes)
 
     def _scan_window(self, n_r, r0, r1, cap, bound, feasible, deadline, sync, hints):
         res = WindowResult(n_r, r0, r1 - r0)

@@ -86,22 +86,28 @@ def test_level_scan_and_replay_match_reference(monkeypatch, name, small, specula
     assert _summary(res) == _expected(doc)
 
 
-@pytest.mark.parametrize("repair,stage", [(True, 8), (True, -1), (False, 8)])
-def test_speculation_mispredictions_are_repaired(monkeypatch, repair, stage):
+@pytest.mark.parametrize("repair,stage,vfirst", [(True, 8, 65536), (True, -1, 65536),
+                                                 (False, 8, 65536), (True, 8, 2)])
+def test_speculation_mispredictions_are_repaired(monkeypatch, repair, stage, vfirst):
     """Tiny budgets make many probes pending; some verify SAT, forcing window
     window repairs (or rescans when a mispredicted candidate had lowered a
     retirement limit) — the result must still be exact."""
+    import paper_2311_15269_b200.engine as E
+
     _patch_decide(monkeypatch)
-    redo = repaired = aborted = 0
+    monkeypatch.setattr(E, "VERIFY_FIRST", vfirst)  # 2: long-probe (decide) path for most
+    redo = repaired = aborted = sp = 0
     for name in CASES:
         doc, res = _run(name, small_windows=True, speculate=True, repair=repair, stage=stage)
         assert _summary(res) == _expected(doc)
         redo += res.report.engine["redo"]
         repaired += res.report.engine["repaired"]
         aborted += res.report.engine["aborted"]
-    print("redo", redo, "repaired", repaired, "aborted", aborted)
+        sp += res.report.engine["sp_probes"]
+    print("redo", redo, "repaired", repaired, "aborted", aborted, "sp", sp)
     assert (repaired if repair else redo) > 0
-    assert aborted > 0  # cancelled verifications were re-run or retired
+    assert aborted > 0 or vfirst < 8  # cancelled verifications were re-run or retired
+    assert sp > 0 or vfirst > 8
 
 
 def _worker(rank, world, port, names, out_dir):
