@@ -193,6 +193,7 @@ def _roofline(kernel_ms: dict, steps: int, workload: str):
     if mp.exists():
         peaks = json.loads(mp.read_text())
     mhz = peaks.get("sm_max_mhz", 1965.0)
+    hbm = peaks.get("hbm_gbs", 6457.4)
     peak = 148 * 4 * mhz * 1e6
     kern = max(kernel_ms, key=kernel_ms.get)
     out = {"bound": "issue", "unit": "warp-inst/s", "peak": peak, "kernel": kern,
@@ -202,12 +203,21 @@ def _roofline(kernel_ms: dict, steps: int, workload: str):
     prof = ROOT / "profiles" / "inst_counts.json"
     if prof.exists():
         d = json.loads(prof.read_text())
-        k = d.get("per_step", {}).get(kern) if d.get("workload") == workload else None
+        ps = d.get("per_step", {}) if d.get("workload") == workload else {}
+        k = ps.get(kern)
         if k and kernel_ms[kern] > 0:
             ach = k["warp_inst"] / (kernel_ms[kern] / steps / 1e3)
             out.update(achieved=ach, frac=ach / peak, traffic=k.get("dram_bytes"),
                        traffic_basis="ncu dram__bytes_read+write per step for this kernel",
                        basis=d.get("basis"))
+        # every timed kernel against the same issue peak (and its HBM bytes)
+        out["kernels"] = {
+            name: {"ms_per_step": ms / steps,
+                   "warp_inst_per_step": ps[name]["warp_inst"],
+                   "issue_frac": ps[name]["warp_inst"] / (ms / steps / 1e3) / peak,
+                   "dram_bytes_per_step": ps[name]["dram_bytes"],
+                   "hbm_frac": ps[name]["dram_bytes"] / (ms / steps / 1e3) / (hbm * 1e9)}
+            for name, ms in kernel_ms.items() if name in ps and ms > 0}
     return out
 
 
@@ -245,7 +255,7 @@ def run_b200_arm(args):
     parity = _matches(res, golden) if args.warmup else None
 
     kernel_ms = 0.0
-    per_kernel = {"k_probe": 0.0, "k_resolve_warp": 0.0, "k_stage": 0.0}
+    per_kernel = {"k_root": 0.0, "k_resolve_warp": 0.0, "k_verify_warp": 0.0, "k_stage": 0.0}
     cands = 0
     walls = []
     stats = {"probes": 0, "nodes": 0, "capped": 0, "root_refuted": 0, "levels": 0}
@@ -257,7 +267,8 @@ def run_b200_arm(args):
         for _ in range(args.steps):
             _flush_l2(torch, dev)               # L2 flushed between timed steps
             e0 = eng.counters.kernel_ms
-            k0 = (eng.counters.probe_ms, eng.counters.resolve_ms, eng.counters.stage_ms)
+            c = eng.counters
+            k0 = (c.root_ms, c.probe_ms + c.resolve_ms, c.verify_ms, c.stage_ms)
             n0 = {k: getattr(eng.counters, k) for k in stats}
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
@@ -265,9 +276,10 @@ def run_b200_arm(args):
             torch.cuda.synchronize(dev)
             walls.append(time.perf_counter() - t0)
             kernel_ms += eng.counters.kernel_ms - e0
-            per_kernel["k_probe"] += eng.counters.probe_ms - k0[0]
-            per_kernel["k_resolve_warp"] += eng.counters.resolve_ms - k0[1]
-            per_kernel["k_stage"] += eng.counters.stage_ms - k0[2]
+            per_kernel["k_root"] += c.root_ms - k0[0]
+            per_kernel["k_resolve_warp"] += c.probe_ms + c.resolve_ms - k0[1]
+            per_kernel["k_verify_warp"] += c.verify_ms - k0[2]
+            per_kernel["k_stage"] += c.stage_ms - k0[3]
             cands += len(res.report.candidates)
             for k in stats:
                 stats[k] += getattr(eng.counters, k) - n0[k]

@@ -184,6 +184,9 @@ void tsl_counters(int64_t *launches, int64_t *h2d_bytes, int64_t *d2h_bytes);
 /* Device time (ms) of the kernels of the last tsl_engine_stage/probe call,
  * measured with CUDA events on the engine's stream. */
 float tsl_engine_last_kernel_ms(tsl_engine *e);
+/* Device time (CUDA events) of the root-filter kernel inside the last
+ * tsl_engine_probe call (part of tsl_engine_last_kernel_ms). */
+float tsl_engine_last_root_ms(tsl_engine *e);
 
 #ifdef __cplusplus
 }

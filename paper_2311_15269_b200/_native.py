@@ -84,7 +84,7 @@ EXPORTS = (
     "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
     "tsl_engine_sat_rows", "tsl_engine_take_deferred", "tsl_engine_add_active",
     "tsl_engine_verify", "tsl_engine_dj",
-    "tsl_engine_last_kernel_ms", "tsl_counters",
+    "tsl_engine_last_kernel_ms", "tsl_engine_last_root_ms", "tsl_counters",
 )
 
 
@@ -134,6 +134,8 @@ def lib():
     L.tsl_counters.argtypes = [vp, vp, vp]
     L.tsl_engine_last_kernel_ms.restype = ctypes.c_float
     L.tsl_engine_last_kernel_ms.argtypes = [vp]
+    L.tsl_engine_last_root_ms.restype = ctypes.c_float
+    L.tsl_engine_last_root_ms.argtypes = [vp]
     _lib = L
     return L
 
@@ -359,3 +361,6 @@ class Engine:
 
     def last_kernel_ms(self) -> float:
         return float(self._L.tsl_engine_last_kernel_ms(self._h))
+
+    def last_root_ms(self) -> float:
+        return float(self._L.tsl_engine_last_root_ms(self._h))

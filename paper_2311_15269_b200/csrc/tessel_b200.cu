@@ -991,8 +991,8 @@ struct tsl_engine {
   int device = 0;
   bool gpu_ready = false;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  float last_ms = 0.f;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;
+  float last_ms = 0.f, last_root_ms = 0.f;  // root_ms: k_root share of the last probe call
   int *d_pool = nullptr;
   // enumeration tables (host copy per n_r, device copy of the staged n_r)
   int h_nr = -1;
@@ -1041,6 +1041,7 @@ struct tsl_engine {
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreate(&evm));
     CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaMalloc(&d_pool, pool.size() * sizeof(int)));
     h2d(d_pool, pool.data(), pool.size() * sizeof(int), stream);
@@ -1113,6 +1114,7 @@ struct tsl_engine {
       if (p) cudaFree(p);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
+    cudaEventDestroy(evm);
     cudaStreamDestroy(stream);
   }
 };
@@ -1348,6 +1350,7 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
   o.counters = e->d_counters;
   o.stats = e->d_stats;
   CK(cudaEventRecord(e->ev0, e->stream));
+  bool root_timed = false;
   if (n_in > 0 && !root_filter_off()) {
     // K2a: warp-per-probe root filter, then the exact DFS on its survivors
     const int wpb = 8;
@@ -1362,6 +1365,8 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
                                                         e->d_act[e->cur], (int)n_in, o,
                                                         e->d_surv, period, icap, widx_limit);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(e->evm, e->stream));
+    root_timed = true;
     // survivors: warp-cooperative reference-exact DFS with the small budget
     // (same outcome contract as k_probe: SAT / settled / deferred)
     const int swpb = 4;
@@ -1397,6 +1402,8 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
   d2h(st, e->d_stats, 8 * sizeof(unsigned long long), e->stream);
   CK(cudaStreamSynchronize(e->stream));
   CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
+  e->last_root_ms = 0.f;
+  if (root_timed) CK(cudaEventElapsedTime(&e->last_root_ms, e->ev0, e->evm));
   e->cur = 1 - e->cur;
   e->n_act = counters[0];
   e->n_def = counters[2];
@@ -1665,5 +1672,6 @@ void tsl_counters(int64_t *launches, int64_t *h2d_bytes, int64_t *d2h_bytes) {
 }
 
 float tsl_engine_last_kernel_ms(tsl_engine *e) { return e ? e->last_ms : 0.f; }
+float tsl_engine_last_root_ms(tsl_engine *e) { return e ? e->last_root_ms : 0.f; }
 
 }  // extern "C"

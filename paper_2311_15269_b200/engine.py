@@ -77,8 +77,10 @@ class EngineCounters:
     aborted: int = 0         # verifications cancelled by a lower SAT
     sp_probes: int = 0       # long probes settled by the subtree-parallel decide
     kernel_ms: float = 0.0
-    probe_ms: float = 0.0     # k_probe (first pass)
-    resolve_ms: float = 0.0   # k_resolve_warp (DJ + warp RX-DFS stages)
+    root_ms: float = 0.0      # k_root (root filter, every probe of a level)
+    probe_ms: float = 0.0     # survivors' small-budget DFS (k_resolve_warp, no filter)
+    resolve_ms: float = 0.0   # k_resolve_warp (disjunctive filter + warp RX-DFS stages)
+    verify_ms: float = 0.0    # k_verify_warp (pending speculated probes)
     stage_ms: float = 0.0     # k_stage (unrank + gate)
     launches: int = 0
     trace: list = field(default_factory=list)
@@ -243,6 +245,8 @@ class BatchedRepetendSearch:
                                "sat": int((st == _native.SAT).sum()), "deferred": 0,
                                "dj_refuted": 0, "dj_nodes": 0},
                               self.eng.last_kernel_ms(), False, (n_r, r0, 0, "verify"))
+            self.counters.resolve_ms -= self.eng.last_kernel_ms()
+            self.counters.verify_ms += self.eng.last_kernel_ms()
             self.counters.verified += len(w)
             again, long = [], []
             for i, (x, q) in enumerate(todo):
@@ -324,6 +328,9 @@ class BatchedRepetendSearch:
             n_sat, widx, rows, n_act, n_def, st = self.eng.probe(
                 period, node_cap, self.small_budget, cap, limit, budget_secs, SAT_CHUNK)
             self.counters.add(st, self.eng.last_kernel_ms(), True, (n_r, r0, period, "probe"))
+            root = self.eng.last_root_ms()
+            self.counters.root_ms += root
+            self.counters.probe_ms -= root
             if deadline and st["capped"] and time.monotonic() > deadline:
                 res.timed_out = True
                 return res, pending

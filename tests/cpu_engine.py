@@ -32,6 +32,9 @@ class OracleEngine:
     def close(self):
         pass
 
+    def last_root_ms(self):
+        return 0.0
+
     def last_kernel_ms(self):
         return 0.0
 
