@@ -62,6 +62,8 @@ WORKLOADS = {
     "C2@3": Workload("C2@3", None, 3, "xshape D=8 1:2, max_nr=3"),
     "C2@4": Workload("C2@4", None, 4, "xshape D=8 1:2, max_nr=4 (parity; CPU 156 s)"),
     "C2@5": Workload("C2@5", None, 5, "xshape D=8 1:2, max_nr=5 (GPU throughput)"),
+    "C2@6": Workload("C2@6", None, 6, "xshape D=8 1:2, max_nr=6 (GPU throughput)"),
+    "C2@8": Workload("C2@8", None, 8, "xshape D=8 1:2, 8 micro-batches (BASELINE configs[1])"),
     "C3@9": Workload("C3@9", 9, None, "mshape D=8 recompute, cap 9 (inflight limit 3)"),
     "C3@12": Workload("C3@12", 12, None, "mshape D=8 recompute, cap 12 (inflight limit 4)"),
     "C4a@3": Workload("C4a@3", None, 3, "nnshape D=8 recompute training, max_nr=3"),
