@@ -188,6 +188,11 @@ float tsl_engine_last_kernel_ms(tsl_engine *e);
  * tsl_engine_probe call (part of tsl_engine_last_kernel_ms). */
 float tsl_engine_last_root_ms(tsl_engine *e);
 
+/* Process-wide counters of the subtree-parallel decide: solves, rounds,
+ * tasks, replays, nested sub-solves, master nodes, master wall ms, task wall
+ * ms (out[8]). */
+void tsl_sp_stats(double *out);
+
 #ifdef __cplusplus
 }
 #endif

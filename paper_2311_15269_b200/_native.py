@@ -84,7 +84,7 @@ EXPORTS = (
     "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
     "tsl_engine_sat_rows", "tsl_engine_take_deferred", "tsl_engine_add_active",
     "tsl_engine_verify", "tsl_engine_dj",
-    "tsl_engine_last_kernel_ms", "tsl_engine_last_root_ms", "tsl_counters",
+    "tsl_engine_last_kernel_ms", "tsl_engine_last_root_ms", "tsl_counters", "tsl_sp_stats",
 )
 
 
@@ -134,6 +134,8 @@ def lib():
     L.tsl_counters.argtypes = [vp, vp, vp]
     L.tsl_engine_last_kernel_ms.restype = ctypes.c_float
     L.tsl_engine_last_kernel_ms.argtypes = [vp]
+    L.tsl_sp_stats.restype = None
+    L.tsl_sp_stats.argtypes = [vp]
     L.tsl_engine_last_root_ms.restype = ctypes.c_float
     L.tsl_engine_last_root_ms.argtypes = [vp]
     _lib = L
@@ -151,6 +153,15 @@ def counters() -> dict:
     v = np.zeros(3, dtype=np.int64)
     lib().tsl_counters(_ptr(v[0:1]), _ptr(v[1:2]), _ptr(v[2:3]))
     return {"launches": int(v[0]), "h2d_bytes": int(v[1]), "d2h_bytes": int(v[2])}
+
+
+def sp_stats() -> dict:
+    """Counters of the subtree-parallel decide (csrc/sp_host.inc)."""
+    a = np.zeros(8, dtype=np.float64)
+    lib().tsl_sp_stats(_ptr(a))
+    keys = ("solves", "rounds", "tasks", "replays", "subsolves", "master_nodes", "master_ms",
+            "task_ms")
+    return {k: float(v) for k, v in zip(keys, a)}
 
 
 def device_count() -> int:

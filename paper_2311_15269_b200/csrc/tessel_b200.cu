@@ -21,7 +21,10 @@
 #include <algorithm>
 #include <chrono>
 #include <ctime>
+#include <functional>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -1673,5 +1676,12 @@ void tsl_counters(int64_t *launches, int64_t *h2d_bytes, int64_t *d2h_bytes) {
 
 float tsl_engine_last_kernel_ms(tsl_engine *e) { return e ? e->last_ms : 0.f; }
 float tsl_engine_last_root_ms(tsl_engine *e) { return e ? e->last_root_ms : 0.f; }
+
+void tsl_sp_stats(double *out) {
+  const SpStats &s = sp_stats();
+  const double v[8] = {(double)s.solves, (double)s.rounds, (double)s.tasks, (double)s.replays,
+                       (double)s.subsolves, (double)s.master_nodes, s.master_ms, s.task_ms};
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
+}
 
 }  // extern "C"

@@ -55,6 +55,17 @@ RESOLVE_STAGES = ((DJ_BUDGET, 32_768), (0, 0))
 # once per window (one concurrent launch); -1 = disjunctive filter only.
 # TESSEL_SPEC_STAGE overrides the RX budget of the single resolve stage.
 SPEC_STAGES = ((DJ_BUDGET, int(os.environ.get("TESSEL_SPEC_STAGE", "65536"))),)
+
+
+def spec_stages(k: int):
+    """The single resolve stage's DFS budget, sized for ~150 ms of warp DFS:
+    64k nodes when every stage fits one lane (K <= 32, ~2.5 us/node), 16k
+    when lanes carry two stages (~8 us/node; measured on C4a@3: 11.7 s vs
+    19.2 s with 64k — its deferred probes are mostly 400k-node TIMEOUTs that
+    the window-end verification settles in one launch)."""
+    if "TESSEL_SPEC_STAGE" in os.environ:
+        return SPEC_STAGES
+    return ((DJ_BUDGET, 65536 if k <= 32 else 16384),)
 TRACE = os.environ.get("TESSEL_TRACE", "0") == "1"
 
 
@@ -131,7 +142,7 @@ class BatchedRepetendSearch:
         self.counters = EngineCounters()
         self.small_budget = int(os.environ.get("TESSEL_SMALL_BUDGET", SMALL_BUDGET))
         self.speculate = os.environ.get("TESSEL_SPECULATE", "1") == "1"
-        self.resolve_stages = SPEC_STAGES if self.speculate else RESOLVE_STAGES
+        self.resolve_stages = spec_stages(k) if self.speculate else RESOLVE_STAGES
         self.repair = os.environ.get("TESSEL_REPAIR", "1") == "1"
         self._last_ms = 0.0
 
