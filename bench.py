@@ -1,9 +1,11 @@
 #!/usr/bin/env python
 """Benchmark: repetend candidates evaluated/s and time-to-optimal of the
-schedule search (BASELINE.json metric) on the X-shape D=8 1:2 workload
-(BASELINE.json configs[1]) at max_nr=4 — the largest C2
-setting the CPU reference finishes, so every step is checked bit-exactly
-against the reference's golden result.
+schedule search (BASELINE.json metric) on BASELINE.json configs[1]: the
+X-shape (Chimera-style) placement, 8 devices, 8 micro-batches (max_nr=8),
+GPT-style fwd:bwd 1:2.  The search ends at the load bound
+t_R = 6 in N_R = 5 after 10.6 M candidates; every step is checked
+bit-exactly against the reference's golden result for the same call
+(tests/golden/search_C2_8.json, ~1 h of the reference's CPU search).
 
 A step = one full ``completion.search()`` (repetend phase over all
 candidates + warmup/cooldown completion).
@@ -44,8 +46,8 @@ os.environ.setdefault("TESSEL_BUDGET_SECS", "1e9")
 BASE = json.loads((ROOT / "BASELINE.json").read_text())
 METRIC = BASE["metric"]
 UNIT = "candidates/s"
-DEFAULT_WORKLOAD = "C2@4"
-GOLDEN = {"C2@4": "C2_4", "C2@3": "C2_3", "C1": "C1", "C3@9": "C3_9", "C5@2": "C5_2",
+DEFAULT_WORKLOAD = "C2@8"
+GOLDEN = {"C2@8": "C2_8", "C2@4": "C2_4", "C2@3": "C2_3", "C1": "C1", "C3@9": "C3_9", "C5@2": "C5_2",
           "C5@3": "C5_3", "C4b": "C4b", "C3@12": "C3_12", "C4a@3": "C4a_3", "C4a@4": "C4a_4"}
 
 

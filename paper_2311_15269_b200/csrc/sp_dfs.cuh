@@ -130,10 +130,23 @@ struct SpSink {
 // task (see the header).  *nodes counts this call's nodes; the cap applies
 // to (*nodes + base_nodes).  Returns RX_SAT / RX_TIMEOUT / SP_EXHAUSTED /
 // SP_PAUSED with depth / v updated.
+// Early stop of a speculative task that can no longer matter: task k's
+// nodes are only ever counted after every earlier task of its round, so once
+// base + pre[k] + (nodes already explored by tasks 0..k-1) exceeds the cap,
+// the probe's verdict is settled before task k (TIMEOUT there, or an earlier
+// task's SAT) and task k stops.  Counts are published every 256 nodes.
+struct SpCut {
+  long long *part;       // per task: nodes explored so far
+  const long long *pre;  // per task: master nodes before it (this walk)
+  long long base, budget;
+  int k;
+};
+
 template <class M>
 __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth, int &v,
                           long long budget, long long base_nodes, long long *nodes_io,
-                          SpSink *sink, long long pause_nodes = 0, int *hist = nullptr) {
+                          SpSink *sink, long long pause_nodes = 0, int *hist = nullptr,
+                          const SpCut *cut = nullptr) {
   const int n = md.n(), cap = md.cap();
   const int lane = wrx_lane();
   long long nodes = *nodes_io;
@@ -244,6 +257,16 @@ __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth,
       break;
     }
     if (hist && lane == 0) ++hist[depth];
+    if (cut && (nodes & 255) == 0) {
+      long long sum = 0;
+      for (int j = lane; j < cut->k; j += 32) sum += ((volatile long long *)cut->part)[j];
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(WRX_FULL, sum, o);
+      if (lane == 0) ((volatile long long *)cut->part)[cut->k] = nodes;
+      if (cut->base + cut->pre[cut->k] + sum > cut->budget) {
+        status = RX_ABORT;
+        break;
+      }
+    }
     {
       int2 *sn = w.snap + (long long)depth * n;
       for (int i = lane; i < n; i += 32) sn[i] = make_int2(w.lo[i], w.hi[i]);

@@ -761,7 +761,9 @@ __global__ void __launch_bounds__(32) k_sp_master(const int *__restrict__ pool, 
 __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
                                                   const int *__restrict__ tasks, int first,
                                                   int count, int split, long long budget,
-                                                  int *snaps, int *results, int *info) {
+                                                  int *snaps, int *results, int *info,
+                                                  long long *part, const long long *pre,
+                                                  long long cut_base, long long cut_budget) {
   extern __shared__ int sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const GenView g = gen_view(pool);
@@ -776,7 +778,10 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
             (const unsigned *)(rec + 3 * n + nw), n);
     int v = rec[3 * n + 2 * nw], depth = rec[3 * n + 2 * nw + 1];
     long long nodes = 0;
-    const int st = sp_explore(g, w, depth, n + 1, depth, v, budget, 0, &nodes, nullptr);
+    const SpCut cut{part, pre, cut_base, cut_budget, (int)t};
+    const int st = sp_explore(g, w, depth, n + 1, depth, v, budget, 0, &nodes, nullptr, 0,
+                              nullptr, cut_budget > 0 ? &cut : nullptr);
+    if (lane == 0 && cut_budget > 0) ((volatile long long *)part)[t] = nodes;
     int *res = results + t * sp_result_words(n);
     bool moved = false;  // S_out != S_in: the master's speculation failed here
     for (int i = lane; i < nw; i += 32) moved |= w.inq[i] != (unsigned)rec[3 * n + nw + i];

@@ -1,2 +1,3 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu.py -x -q -k "nested_runs" --durations=4 2>&1 | tail -8 > gpurun_out/pytest_iter.log
+timeout 600 python scripts/phase_probe.py C2@8 > gpurun_out/phase_c2_8.log 2>&1
+timeout 600 python scripts/phase_probe.py C3@12 > gpurun_out/phase_c3_12.log 2>&1
