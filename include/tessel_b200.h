@@ -188,6 +188,22 @@ float tsl_engine_last_kernel_ms(tsl_engine *e);
  * tsl_engine_probe call (part of tsl_engine_last_kernel_ms). */
 float tsl_engine_last_root_ms(tsl_engine *e);
 
+/* Schedule validation on the device — the checks of the reference's
+ * validate_schedule (schedule.py:77-168) for an N-micro-batch schedule:
+ * starts[st * N + n]; deps as sorted (a, b) pairs.  P = next power of two
+ * >= max over devices of (#stages on the device) * N.  Writes the number of
+ * violations (overlaps + memory group ends + dependencies + negative starts)
+ * to *out_count and, only when it is > 0, per device d the sorted event keys
+ * ((start ^ 0x80000000) << 32 | position, position = stage-slot * N + mb,
+ * stage slots ascending) and, at sorted position p, overlap / memory flags
+ * and the running memory after p (D*P each), dependency flags [n_deps*N] and
+ * negative-start flags [K*N].  The caller formats the violation list. */
+int tsl_validate(int K, int D, const int32_t *dur, const int32_t *mem, const uint64_t *devmask,
+                 int n_deps, const int32_t *deps, int N, const int32_t *starts,
+                 const int64_t *init_mem, int64_t cap, int64_t P, int64_t *out_count,
+                 uint64_t *sorted_keys, uint8_t *overlap_flags, uint8_t *memory_flags,
+                 int64_t *runs, uint8_t *dep_flags, uint8_t *neg_flags);
+
 /* Process-wide counters of the subtree-parallel decide: solves, rounds,
  * tasks, replays, nested sub-solves, master nodes, master wall ms, task wall
  * ms (out[8]). */

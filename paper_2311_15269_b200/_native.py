@@ -83,7 +83,7 @@ EXPORTS = (
     "tsl_decide_batch", "tsl_engine_open", "tsl_engine_close", "tsl_engine_count",
     "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
     "tsl_engine_sat_rows", "tsl_engine_take_deferred", "tsl_engine_add_active",
-    "tsl_engine_verify", "tsl_engine_dj",
+    "tsl_engine_verify", "tsl_engine_dj", "tsl_validate",
     "tsl_engine_last_kernel_ms", "tsl_engine_last_root_ms", "tsl_counters", "tsl_sp_stats",
 )
 
@@ -134,6 +134,9 @@ def lib():
     L.tsl_counters.argtypes = [vp, vp, vp]
     L.tsl_engine_last_kernel_ms.restype = ctypes.c_float
     L.tsl_engine_last_kernel_ms.argtypes = [vp]
+    L.tsl_validate.restype = i32
+    L.tsl_validate.argtypes = [i32, i32, vp, vp, vp, i32, vp, i32, vp, vp, i64, i64, vp, vp, vp,
+                               vp, vp, vp, vp]
     L.tsl_sp_stats.restype = None
     L.tsl_sp_stats.argtypes = [vp]
     L.tsl_engine_last_root_ms.restype = ctypes.c_float

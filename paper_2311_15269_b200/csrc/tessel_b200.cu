@@ -36,6 +36,7 @@
 #include "wrx_dfs.cuh"
 #include "wdj_solve.cuh"
 #include "sp_dfs.cuh"
+#include "validate.cuh"
 
 #define TSL_VERSION 2
 
@@ -829,6 +830,18 @@ struct DecideCtx {
 DecideCtx &decide_ctx() {
   static DecideCtx ctx;
   return ctx;
+}
+
+cudaStream_t decide_ctx_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  static thread_local int dev = -1;
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  if (!s || dev != d) {
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    dev = d;
+  }
+  return s;
 }
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -1669,6 +1682,92 @@ int tsl_engine_dj(tsl_engine *e, int64_t count, const int32_t *assignments,
   d2h(nodes_out, d_n, count * sizeof(long long), e->stream);
   CK(cudaStreamSynchronize(e->stream));
   for (void *p : {(void *)d_a, (void *)d_p, (void *)d_st, (void *)d_n, (void *)d_g}) cudaFree(p);
+  return TSL_OK;
+  API_END
+}
+
+int tsl_validate(int K, int D, const int32_t *dur, const int32_t *mem, const uint64_t *devmask,
+                 int n_deps, const int32_t *deps, int N, const int32_t *starts,
+                 const int64_t *init_mem, int64_t cap, int64_t P, int64_t *out_count,
+                 uint64_t *sorted_keys, uint8_t *overlap_flags, uint8_t *memory_flags,
+                 int64_t *runs, uint8_t *dep_flags, uint8_t *neg_flags) {
+  API_BEGIN
+  require_device();
+  if (K < 1 || D < 1 || D > TSL_MAX_DEVICES || N < 1) throw tsl::Error(TSL_EINVAL, "bad sizes");
+  std::vector<int> dptr(D + 1, 0), dst;
+  long long maxE = 0;
+  for (int d = 0; d < D; ++d) {
+    for (int st = 0; st < K; ++st)
+      if ((devmask[st] >> d) & 1) dst.push_back(st);
+    dptr[d + 1] = (int)dst.size();
+    maxE = std::max(maxE, (long long)(dptr[d + 1] - dptr[d]) * N);
+  }
+  long long want = 1;
+  while (want < std::max(maxE, 1LL)) want <<= 1;
+  if (P != want) throw tsl::Error(TSL_EINVAL, "P must be the next power of two >= max events/device");
+  if (dst.empty()) dst.push_back(0);
+  cudaStream_t s = decide_ctx_stream();
+  const long long KN = (long long)K * N, DP = (long long)D * P;
+  const long long nd = std::max(n_deps, 1);
+  int *d_starts, *d_dptr, *d_dst, *d_dur, *d_mem, *d_deps;
+  long long *d_init, *d_runs;
+  unsigned long long *d_keys, *d_count;
+  unsigned char *d_ov, *d_mf, *d_depf, *d_negf;
+  CK(cudaMalloc(&d_starts, KN * sizeof(int)));
+  CK(cudaMalloc(&d_dptr, (D + 1) * sizeof(int)));
+  CK(cudaMalloc(&d_dst, dst.size() * sizeof(int)));
+  CK(cudaMalloc(&d_dur, K * sizeof(int)));
+  CK(cudaMalloc(&d_mem, K * sizeof(int)));
+  CK(cudaMalloc(&d_deps, 2 * nd * sizeof(int)));
+  CK(cudaMalloc(&d_init, D * sizeof(long long)));
+  CK(cudaMalloc(&d_runs, DP * sizeof(long long)));
+  CK(cudaMalloc(&d_keys, DP * sizeof(unsigned long long)));
+  CK(cudaMalloc(&d_count, sizeof(unsigned long long)));
+  CK(cudaMalloc(&d_ov, DP));
+  CK(cudaMalloc(&d_mf, DP));
+  CK(cudaMalloc(&d_depf, nd * N));
+  CK(cudaMalloc(&d_negf, KN));
+  h2d(d_starts, starts, KN * sizeof(int), s);
+  h2d(d_dptr, dptr.data(), (D + 1) * sizeof(int), s);
+  h2d(d_dst, dst.data(), dst.size() * sizeof(int), s);
+  h2d(d_dur, dur, K * sizeof(int), s);
+  h2d(d_mem, mem, K * sizeof(int), s);
+  if (n_deps > 0) h2d(d_deps, deps, 2 * n_deps * sizeof(int), s);
+  h2d(d_init, init_mem, D * sizeof(long long), s);
+  CK(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
+  const int T = 256;
+  COUNT_LAUNCH();
+  k_val_keys<<<(int)((DP + T - 1) / T), T, 0, s>>>(d_starts, d_dptr, d_dst, D, N, P, d_keys);
+  for (long long k = 2; k <= P; k <<= 1)
+    for (long long j = k >> 1; j > 0; j >>= 1) {
+      COUNT_LAUNCH();
+      k_val_bitonic<<<(int)((DP + T - 1) / T), T, 0, s>>>(d_keys, DP, P, k, j);
+    }
+  COUNT_LAUNCH();
+  k_val_scan<<<D, 1024, 0, s>>>(d_keys, d_dptr, d_dst, d_dur, d_mem, N, P, d_init, cap, d_ov,
+                                d_mf, d_runs, d_count);
+  const long long items = std::max(KN, nd * N);
+  COUNT_LAUNCH();
+  k_val_items<<<(int)((items + T - 1) / T), T, 0, s>>>(d_starts, d_dur, d_deps, n_deps, K, N,
+                                                        d_depf, d_negf, d_count);
+  CK(cudaGetLastError());
+  unsigned long long cnt = 0;
+  d2h(&cnt, d_count, sizeof cnt, s);
+  CK(cudaStreamSynchronize(s));
+  *out_count = (int64_t)cnt;
+  if (cnt) {
+    d2h(sorted_keys, d_keys, DP * sizeof(unsigned long long), s);
+    d2h(overlap_flags, d_ov, DP, s);
+    d2h(memory_flags, d_mf, DP, s);
+    d2h(runs, d_runs, DP * sizeof(long long), s);
+    if (n_deps > 0) d2h(dep_flags, d_depf, (long long)n_deps * N, s);
+    d2h(neg_flags, d_negf, KN, s);
+    CK(cudaStreamSynchronize(s));
+  }
+  for (void *p : {(void *)d_starts, (void *)d_dptr, (void *)d_dst, (void *)d_dur, (void *)d_mem,
+                  (void *)d_deps, (void *)d_init, (void *)d_runs, (void *)d_keys,
+                  (void *)d_count, (void *)d_ov, (void *)d_mf, (void *)d_depf, (void *)d_negf})
+    cudaFree(p);
   return TSL_OK;
   API_END
 }
