@@ -40,6 +40,11 @@
 
 #define TSL_VERSION 2
 
+// resident blocks per SM the resolve kernel is compiled for (register cap)
+#ifndef RESOLVE_MIN_BLOCKS
+#define RESOLVE_MIN_BLOCKS 4
+#endif
+
 static thread_local std::string g_err;
 
 // Process-wide accounting for the bench's gpu_launches / e2e byte counts.
@@ -459,7 +464,7 @@ __host__ __device__ inline int rep_warp_smem_words(const int *pool) {
          (pool[R_NDEP] > 0 ? pool[R_NDEP] : 1) + pool[R_D] + 2;
 }
 
-__global__ void __launch_bounds__(128) k_resolve_warp(const int *__restrict__ gpool,
+__global__ void __launch_bounds__(128, RESOLVE_MIN_BLOCKS) k_resolve_warp(const int *__restrict__ gpool,
                                                       const unsigned char *__restrict__ assign,
                                                       const int *__restrict__ def_in, int n_def,
                                                       const int *__restrict__ n_def_dev,
