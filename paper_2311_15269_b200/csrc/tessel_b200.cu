@@ -597,6 +597,67 @@ __global__ void __launch_bounds__(128, RESOLVE_MIN_BLOCKS) k_resolve_warp(const 
   }
 }
 
+// Disjunctive filter alone (wdj_solve.cuh), one warp per deferred probe with
+// a small shared footprint so many warps hide its latency: refuted probes
+// stay active (exactly "not SAT", see k_resolve); the others go to `keep`
+// (count in o.counters[3]) for the reference-exact DFS stage.  Probes above
+// the speculative limit (a SAT found meanwhile) are kept too.
+__host__ __device__ inline int dj_warp_words(const int *pool) {
+  const int ndep1 = pool[R_NDEP] > 0 ? pool[R_NDEP] : 1;
+  return (wdj_smem_words(pool[R_K], pool[R_NPAIR]) + ndep1 + pool[R_D] + 3) & ~3;
+}
+
+__global__ void __launch_bounds__(256, 4) k_dj_filter(const int *__restrict__ gpool,
+                                                   const unsigned char *__restrict__ assign,
+                                                   const int *__restrict__ def_in, int n_def,
+                                                   ProbeOut o, int *__restrict__ keep, int P,
+                                                   long long dj_budget, int cap,
+                                                   long long widx_limit, int *gscratch,
+                                                   long long gwords, const int *dev_limit) {
+  extern __shared__ int sp[];
+  load_pool(sp, gpool);
+  const int K = sp[R_K];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int ndep1 = sp[R_NDEP] > 0 ? sp[R_NDEP] : 1;
+  int *mine = sp + ((sp[R_WORDS] + 3) & ~3) + wib * dj_warp_words(sp);
+  int *deplag = mine + wdj_smem_words(K, sp[R_NPAIR]);
+  int *init = deplag + ndep1;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  WdjWs w = wdj_carve(mine, gscratch + gw * gwords, K, sp[R_NPAIR]);
+  unsigned long long s_dju = 0, s_djn = 0;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long t = gw; t < n_def; t += nwarps) {
+    const int widx = def_in[t];
+    if (widx > widx_limit) continue;
+    int l = 0;
+    if (lane == 0) l = dev_limit ? *(volatile const int *)dev_limit : 0x7fffffff;
+    l = __shfl_sync(WRX_FULL, l, 0);
+    int dj = DJ_UNKNOWN;
+    if (widx <= l) {
+      const unsigned char *a = assign + (long long)widx * K;
+      if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
+      for (int i = lane; i < K; i += 32) w.av[i] = a[i];
+      __syncwarp();
+      long long dn = 0;
+      dj = wdj_decide(sp, P, cap, init, w, dj_budget, &dn);
+      s_djn += (unsigned long long)dn;
+    }
+    if (lane == 0) {
+      if (dj == DJ_UNSAT) {
+        ++s_dju;
+        o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
+      } else {
+        keep[atomicAdd(&o.counters[3], 1)] = widx;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && (s_dju || s_djn)) {
+    atomicAdd(&o.stats[6], s_dju);
+    atomicAdd(&o.stats[7], s_djn);
+  }
+}
+
 // Verification of speculated probes: explicit (window index, period)
 // pairs, one warp each, reference-exact DFS under the reference cap for that
 // period (0 = none at the load bound).  Writes status / nodes / starts per
@@ -870,6 +931,15 @@ bool dj_mode_warp(const int *pool) {
   if (m && std::string(m) == "lane") return false;
   return wdj_smem_words(pool[R_K], pool[R_NPAIR]) <= wrx_snap_words(pool[R_K]) &&
          wdj_snap_words(pool[R_K], pool[R_NPAIR]) <= 32 * rep_ws_words(pool);
+}
+
+// TSL_DJ_SPLIT=1 runs the disjunctive filter as its own high-occupancy
+// launch before the DFS stage.  Off by default: measured slower on C2@4/@8
+// (the filter is not occupancy-bound, and the split serialises the DFS of a
+// SAT probe behind the whole filter launch).
+bool dj_split() {
+  const char *m = getenv("TSL_DJ_SPLIT");
+  return m && std::string(m) == "1";
 }
 
 bool decide_mode_warp() {
@@ -1468,6 +1538,31 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
   o.counters = e->d_counters;
   o.stats = e->d_stats;
   CK(cudaEventRecord(e->ev0, e->stream));
+  const int *rx_in = e->d_def[e->dcur];
+  const int *rx_count = nullptr;
+  if (n_def > 0 && decide_mode_warp() && dj_budget > 0 && dj_mode_warp(e->pool.data()) &&
+      dj_split()) {
+    // the filter alone first, at high occupancy; its survivors (d_surv,
+    // counters[3]) then take the DFS stage below without the filter
+    const int wpb = 8;
+    const long long gwords = wdj_snap_words(e->pool[R_K], e->pool[R_NPAIR]) + 8;
+    long long dblocks = std::max(1LL, std::min<long long>((n_def + wpb - 1) / wpb,
+                                                          (long long)e->num_sms * 4));
+    dblocks = std::min<long long>(dblocks, (e->ws_threads * e->ws_words) / (gwords * wpb));
+    const size_t smem = (size_t)(((e->pool.size() + 3) & ~(size_t)3) +
+                                 wpb * dj_warp_words(e->pool.data())) * sizeof(int);
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_dj_filter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+    COUNT_LAUNCH();
+    k_dj_filter<<<(int)dblocks, 32 * wpb, smem, e->stream>>>(
+        e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, o, e->d_surv, period,
+        dj_budget, icap, widx_limit, e->d_ws, gwords, e->d_counters + 4);
+    CK(cudaGetLastError());
+    rx_in = e->d_surv;
+    rx_count = e->d_counters + 3;
+    dj_budget = 0;
+  }
   if (n_def > 0 && decide_mode_warp()) {
     const int wpb = 4;
     long long wblocks = (n_def + wpb - 1) / wpb;
@@ -1480,7 +1575,7 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
                               (int)smem));
     COUNT_LAUNCH();
     k_resolve_warp<<<(int)wblocks, 32 * wpb, smem, e->stream>>>(
-        e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, nullptr, o, period,
+        e->d_pool, e->d_assign, rx_in, (int)n_def, rx_count, o, period,
         node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? -1 : stage_budget,
         dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words,
         e->d_counters + 4, dj_mode_warp(e->pool.data()) ? 1 : 0);
