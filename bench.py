@@ -170,7 +170,7 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(walls), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {w.note}", "max_nr": w.max_nr,
                    "mem_capacity": w.mem_capacity,
                    "sample": f"search() with budget={args.ref_sample_secs}s per step"},
