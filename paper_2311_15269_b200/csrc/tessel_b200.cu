@@ -85,6 +85,20 @@ static void d2h(void *dst, const void *src, size_t bytes, cudaStream_t s) {
   COUNT_D2H(bytes);
 }
 
+// Frees temporary device buffers on every exit path (including errors).
+struct DevFree {
+  std::vector<void *> ptrs;
+  template <class T>
+  T *add(T *p) {
+    ptrs.push_back((void *)p);
+    return p;
+  }
+  ~DevFree() {
+    for (void *p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
 static void require_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -1762,11 +1776,17 @@ int tsl_engine_dj(tsl_engine *e, int64_t count, const int32_t *assignments,
                           dj_ws_words(K, D, e->pool[R_NPAIR], e->pool[R_MAXDI])) + 8;
   int *d_a = nullptr, *d_p = nullptr, *d_st = nullptr, *d_g = nullptr;
   long long *d_n = nullptr;
+  DevFree guard;
   CK(cudaMalloc(&d_a, count * K * sizeof(int)));
+  guard.add(d_a);
   CK(cudaMalloc(&d_p, count * sizeof(int)));
+  guard.add(d_p);
   CK(cudaMalloc(&d_st, count * sizeof(int)));
+  guard.add(d_st);
   CK(cudaMalloc(&d_n, count * sizeof(long long)));
+  guard.add(d_n);
   CK(cudaMalloc(&d_g, warps * gwords * sizeof(int)));
+  guard.add(d_g);
   h2d(d_a, assignments, count * K * sizeof(int), e->stream);
   h2d(d_p, period, count * sizeof(int), e->stream);
   const int ndep1 = e->pool[R_NDEP] > 0 ? e->pool[R_NDEP] : 1;
@@ -1781,7 +1801,6 @@ int tsl_engine_dj(tsl_engine *e, int64_t count, const int32_t *assignments,
   d2h(status_out, d_st, count * sizeof(int), e->stream);
   d2h(nodes_out, d_n, count * sizeof(long long), e->stream);
   CK(cudaStreamSynchronize(e->stream));
-  for (void *p : {(void *)d_a, (void *)d_p, (void *)d_st, (void *)d_n, (void *)d_g}) cudaFree(p);
   return TSL_OK;
   API_END
 }
@@ -1813,20 +1832,35 @@ int tsl_validate(int K, int D, const int32_t *dur, const int32_t *mem, const uin
   long long *d_init, *d_runs;
   unsigned long long *d_keys, *d_count;
   unsigned char *d_ov, *d_mf, *d_depf, *d_negf;
+  DevFree guard;
   CK(cudaMalloc(&d_starts, KN * sizeof(int)));
+  guard.add(d_starts);
   CK(cudaMalloc(&d_dptr, (D + 1) * sizeof(int)));
+  guard.add(d_dptr);
   CK(cudaMalloc(&d_dst, dst.size() * sizeof(int)));
+  guard.add(d_dst);
   CK(cudaMalloc(&d_dur, K * sizeof(int)));
+  guard.add(d_dur);
   CK(cudaMalloc(&d_mem, K * sizeof(int)));
+  guard.add(d_mem);
   CK(cudaMalloc(&d_deps, 2 * nd * sizeof(int)));
+  guard.add(d_deps);
   CK(cudaMalloc(&d_init, D * sizeof(long long)));
+  guard.add(d_init);
   CK(cudaMalloc(&d_runs, DP * sizeof(long long)));
+  guard.add(d_runs);
   CK(cudaMalloc(&d_keys, DP * sizeof(unsigned long long)));
+  guard.add(d_keys);
   CK(cudaMalloc(&d_count, sizeof(unsigned long long)));
+  guard.add(d_count);
   CK(cudaMalloc(&d_ov, DP));
+  guard.add(d_ov);
   CK(cudaMalloc(&d_mf, DP));
+  guard.add(d_mf);
   CK(cudaMalloc(&d_depf, nd * N));
+  guard.add(d_depf);
   CK(cudaMalloc(&d_negf, KN));
+  guard.add(d_negf);
   h2d(d_starts, starts, KN * sizeof(int), s);
   h2d(d_dptr, dptr.data(), (D + 1) * sizeof(int), s);
   h2d(d_dst, dst.data(), dst.size() * sizeof(int), s);
@@ -1864,10 +1898,6 @@ int tsl_validate(int K, int D, const int32_t *dur, const int32_t *mem, const uin
     d2h(neg_flags, d_negf, KN, s);
     CK(cudaStreamSynchronize(s));
   }
-  for (void *p : {(void *)d_starts, (void *)d_dptr, (void *)d_dst, (void *)d_dur, (void *)d_mem,
-                  (void *)d_deps, (void *)d_init, (void *)d_runs, (void *)d_keys,
-                  (void *)d_count, (void *)d_ov, (void *)d_mf, (void *)d_depf, (void *)d_negf})
-    cudaFree(p);
   return TSL_OK;
   API_END
 }
