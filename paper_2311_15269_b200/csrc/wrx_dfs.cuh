@@ -159,9 +159,11 @@ __device__ bool wrx_propagate(const M &md, WWs &w, int &qh, int &qt, int &qc) {
 
 
 // ---- warp sort / scan helpers (one element per lane, 32 lanes) --------
-__device__ __forceinline__ void wrx_bitonic(unsigned long long &key, int &p0, int &p1) {
+// W = power-of-two width (8, 16 or 32): sorts every aligned group of W lanes
+__device__ __forceinline__ void wrx_bitonic(unsigned long long &key, int &p0, int &p1,
+                                            int W = 32) {
   const int lane = wrx_lane();
-  for (int size = 2; size <= 32; size <<= 1) {
+  for (int size = 2; size <= W; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       const unsigned long long pk = __shfl_xor_sync(WRX_FULL, key, stride);
       const int q0 = __shfl_xor_sync(WRX_FULL, p0, stride);
@@ -176,33 +178,34 @@ __device__ __forceinline__ void wrx_bitonic(unsigned long long &key, int &p0, in
     }
   }
 }
-__device__ __forceinline__ int wrx_scan_add(int v) {  // inclusive prefix sum
+// scans over W lanes: exact for lanes < W when lanes >= k hold identities
+__device__ __forceinline__ int wrx_scan_add(int v, int W = 32) {  // inclusive prefix sum
   const int lane = wrx_lane();
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < W; o <<= 1) {
     const int t = __shfl_up_sync(WRX_FULL, v, o);
     if (lane >= o) v += t;
   }
   return v;
 }
-__device__ __forceinline__ int wrx_rscan_add(int v) {  // inclusive suffix sum
+__device__ __forceinline__ int wrx_rscan_add(int v, int W = 32) {  // inclusive suffix sum
   const int lane = wrx_lane();
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < W; o <<= 1) {
     const int t = __shfl_down_sync(WRX_FULL, v, o);
     if (lane + o < 32) v += t;
   }
   return v;
 }
-__device__ __forceinline__ int wrx_rscan_max(int v) {
+__device__ __forceinline__ int wrx_rscan_max(int v, int W = 32) {
   const int lane = wrx_lane();
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < W; o <<= 1) {
     const int t = __shfl_down_sync(WRX_FULL, v, o);
     if (lane + o < 32) v = t > v ? t : v;
   }
   return v;
 }
-__device__ __forceinline__ int wrx_scan_min(int v) {
+__device__ __forceinline__ int wrx_scan_min(int v, int W = 32) {
   const int lane = wrx_lane();
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < W; o <<= 1) {
     const int t = __shfl_up_sync(WRX_FULL, v, o);
     if (lane >= o) v = t < v ? t : v;
   }
@@ -216,7 +219,7 @@ __device__ __forceinline__ unsigned long long wrx_key(int v, int tie) {
 // _mem_ok for a device with k <= 32 items: sort events by time, prefix sums,
 // check the running sum at the end of every equal-time group.
 template <class M>
-__device__ bool wrx_mem_ok32(const M &md, WWs &w, int d, int cap, int pb, int k) {
+__device__ bool wrx_mem_ok32(const M &md, WWs &w, int d, int cap, int pb, int k, int W) {
   const int lane = wrx_lane();
   const int init = md.init_mem(d);
   unsigned long long key = ~0ull;
@@ -230,8 +233,8 @@ __device__ bool wrx_mem_ok32(const M &md, WWs &w, int d, int cap, int pb, int k)
       m = mm;
     }
   }
-  wrx_bitonic(key, m, dummy);
-  const int run = init + wrx_scan_add(m);
+  wrx_bitonic(key, m, dummy, W);
+  const int run = init + wrx_scan_add(m, W);
   const unsigned long long nkey = __shfl_down_sync(WRX_FULL, key, 1);
   const bool valid = key != ~0ull;
   const bool group_end = valid && (lane == 31 || nkey == ~0ull || (nkey >> 32) != (key >> 32));
@@ -242,7 +245,7 @@ __device__ bool wrx_mem_ok32(const M &md, WWs &w, int d, int cap, int pb, int k)
 // (e, a-rank) by bitonic sorts; serial completion, suffix and prefix
 // energetic checks by scans.
 template <class M>
-__device__ bool wrx_dev_ok32(const M &md, WWs &w, int pb, int k) {
+__device__ bool wrx_dev_ok32(const M &md, WWs &w, int pb, int k, int W) {
   const int lane = wrx_lane();
   const bool real = lane < k;
   int a = 0, du = 0, e = -(1 << 30);
@@ -257,11 +260,11 @@ __device__ bool wrx_dev_ok32(const M &md, WWs &w, int pb, int k) {
   const int sd = __reduce_add_sync(WRX_FULL, du);
   unsigned long long key = real ? wrx_key(a, lane) : ~0ull;
   int pd = du, pe = e;
-  wrx_bitonic(key, pd, pe);  // lane = rank in the stable a-order
+  wrx_bitonic(key, pd, pe, W);  // lane = rank in the stable a-order
   const bool r2 = key != ~0ull;
   const int ra = (int)(key >> 32) - (1 << 30);
-  const int suf_d = wrx_rscan_add(pd);
-  const int suf_e = wrx_rscan_max(pe);
+  const int suf_d = wrx_rscan_add(pd, W);
+  const int suf_e = wrx_rscan_max(pe, W);
   bool bad = r2 && (ra + suf_d > suf_e);
   int c = r2 ? ra + suf_d : sd;
   c = __reduce_max_sync(WRX_FULL, c > sd ? c : sd);
@@ -269,11 +272,11 @@ __device__ bool wrx_dev_ok32(const M &md, WWs &w, int pb, int k) {
   // stable e-order of the a-sorted sequence: key (e, a-rank)
   unsigned long long key2 = r2 ? wrx_key(pe, lane) : ~0ull;
   int qa = r2 ? ra : (1 << 30), qd = r2 ? pd : 0;
-  wrx_bitonic(key2, qa, qd);
+  wrx_bitonic(key2, qa, qd, W);
   const bool r3 = key2 != ~0ull;
   const int qe = (int)(key2 >> 32) - (1 << 30);
-  const int pre_d = wrx_scan_add(qd);
-  const int pre_a = wrx_scan_min(qa);
+  const int pre_d = wrx_scan_add(qd, W);
+  const int pre_a = wrx_scan_min(qa, W);
   bad |= r3 && (pre_a + pre_d > qe);
   return !__any_sync(WRX_FULL, bad);
 }
@@ -287,7 +290,8 @@ __device__ bool wrx_mem_ok(const M &md, WWs &w, int d, int cap) {
   const int init = md.init_mem(d);
   if (init > cap) return false;
   const int pb = md.dev_begin(d), k = md.dev_end(d) - pb;
-  if (k > 8 && k <= 32) return wrx_mem_ok32(md, w, d, cap, pb, k);
+  // small devices: the O(k^2) shared-memory form measured faster than a sort
+  if (k > 8 && k <= 32) return wrx_mem_ok32(md, w, d, cap, pb, k, k <= 16 ? 16 : 32);
   const int lane = wrx_lane();
   for (int i = lane; i < k; i += 32) {
     const int it = md.dev_item(pb + i);
@@ -317,7 +321,7 @@ template <class M>
 __device__ bool wrx_dev_ok(const M &md, WWs &w, int d) {
   const int pb = md.dev_begin(d), k = md.dev_end(d) - pb;
   if (k == 0) return true;
-  if (k > 8 && k <= 32) return wrx_dev_ok32(md, w, pb, k);
+  if (k > 8 && k <= 32) return wrx_dev_ok32(md, w, pb, k, k <= 16 ? 16 : 32);
   const int lane = wrx_lane();
   int lim = -(1 << 30), sd = 0;
   for (int i = lane; i < k; i += 32) {

@@ -217,7 +217,8 @@ def main(names):
             w = WORKLOADS[name]
             if name in ("C2@5", "C5@4"):
                 continue  # the CPU reference does not finish these
-            run_search(name.replace("@", "_"), w.placement(), w.mem_capacity, w.max_nr, record=True)
+            run_search(name.replace("@", "_"), w.placement(), w.mem_capacity, w.max_nr,
+                       record=os.environ.get("GOLDEN_NO_RECORD") != "1")
         else:
             raise SystemExit(f"unknown golden {name}")
 

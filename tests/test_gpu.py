@@ -121,8 +121,12 @@ def _check(doc, res):
 
 
 FAST = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "m4_cap8", "k4_k3", "v2_k4", "nn4_k3",
-        "C1", "C2_3", "C3_9", "C5_2"]
-SLOW_CASES = ["C2_4", "C3_12", "C4a_3", "C4a_4", "C4b", "C5_3"]
+        "C1", "C2_3", "C3_9", "C5_2",
+        # the full-size parity configs — seconds each on the B200
+        "C2_4", "C3_12", "C4a_3", "C4a_4", "C4b", "C5_3"]
+# BASELINE configs[1] (8 micro-batches): its reference golden takes the CPU
+# reference hours; checked when tests/golden/search_C2_8.json is present
+SLOW_CASES = ["C2_8"]
 
 
 @pytest.mark.parametrize("name", FAST)
@@ -135,11 +139,8 @@ def test_search_matches_reference(gpu, name):
     _check(doc, search(p, doc["mem_capacity"], max_nr=doc["max_nr"]))
 
 
-@pytest.mark.slow
 @pytest.mark.parametrize("name", SLOW_CASES)
 def test_search_matches_reference_full_configs(gpu, name):
-    if not SLOW:
-        pytest.skip("set TESSEL_SLOW=1 for the full-size parity configs")
     if not (GOLDEN / f"search_{name}.json").exists():
         pytest.skip("golden not generated")
     from paper_2311_15269_b200.completion import search
