@@ -72,4 +72,5 @@ WORKLOADS = {
     "C5@2": Workload("C5@2", None, 2, "kshape D=16 heterogeneous, max_nr=2"),
     "C5@3": Workload("C5@3", None, 3, "kshape D=16 heterogeneous, max_nr=3"),
     "C5@4": Workload("C5@4", None, 4, "kshape D=16 heterogeneous, max_nr=4 (GPU only)"),
+    "C5@5": Workload("C5@5", None, 5, "kshape D=16 heterogeneous, max_nr=5 (GPU only)"),
 }
