@@ -15,7 +15,7 @@ from . import placement, schedule  # noqa: F401  (pure data model, importable wi
 def __getattr__(name):
     # compute modules load the native library lazily
     if name in ("repetend", "solver", "completion", "engine", "_core", "_native", "workloads",
-                "parallel", "to_search", "extension", "validate"):
+                "parallel", "to_search", "extension", "validate", "emitter", "simulator"):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)
