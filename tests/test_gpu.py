@@ -331,3 +331,20 @@ def test_subtree_parallel_nested_runs_exact(gpu, monkeypatch, helpers):
     for p in probes:
         got = gpu.decide_batch([_problem(p)])[0]
         assert got == (p["status"], p["starts"], p["nodes"]), p["n"]
+
+
+@pytest.mark.parametrize("env", [{"TSL_DJ_SPLIT": "1"}, {"TSL_SP_PIPELINE": "0"},
+                                 {"TSL_ROOT_FILTER": "0"}])
+def test_search_variants_match_reference(gpu, monkeypatch, env):
+    """The non-default execution variants kept for cross-validation (split
+    disjunctive-filter launch, no pipelined SP master walk, thread-per-probe
+    level pass) give the same searches."""
+    from paper_2311_15269_b200.completion import search
+    from paper_2311_15269_b200.placement import placement_from_dict
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for name in ("C2_3", "C5_2", "C3_9", "m4_cap8"):
+        doc = load_search(name)
+        p = placement_from_dict(doc["placement"])
+        _check(doc, search(p, doc["mem_capacity"], max_nr=doc["max_nr"]))
