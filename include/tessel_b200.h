@@ -159,6 +159,20 @@ int tsl_engine_add_active(tsl_engine *e, int64_t count, const int64_t *widx);
  * with w2 > w and P2 >= P: such pairs stop early with status 3 (aborted, not
  * a reference status); the caller re-runs them unless that SAT's completion
  * check passes. */
+/* Asynchronous verification (engine.py pipelines windows): stash the
+ * assignments of `count` window indices of the staged window into slot 0/1
+ * (rows = positions 0..count-1), launch the verification of (row position,
+ * window index, period, cap) quadruples of that slot on the engine's
+ * verification stream — it runs while the next window is staged and
+ * scanned — and wait for / read its results (same meaning as
+ * tsl_engine_verify). */
+int tsl_engine_verify_stash(tsl_engine *e, int slot, int64_t count, const int64_t *widx);
+int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64_t *pos,
+                             const int64_t *widx, const int32_t *period,
+                             const int64_t *node_budget, int64_t cap);
+int tsl_engine_verify_wait(tsl_engine *e, int slot, int32_t *status_out, int64_t *nodes_out,
+                           int32_t *starts_out);
+
 /* Diagnostic: the disjunctive filter (DJ) on explicit (assignment[K],
  * period) pairs — status 0 = proven infeasible, 1 = feasible, 2 = undecided
  * within `budget` orientation nodes.  mode 1 = warp filter, 0 = one-lane

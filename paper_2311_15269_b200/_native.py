@@ -83,7 +83,8 @@ EXPORTS = (
     "tsl_decide_batch", "tsl_engine_open", "tsl_engine_close", "tsl_engine_count",
     "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
     "tsl_engine_sat_rows", "tsl_engine_take_deferred", "tsl_engine_add_active",
-    "tsl_engine_verify", "tsl_engine_dj", "tsl_validate",
+    "tsl_engine_verify", "tsl_engine_verify_stash", "tsl_engine_verify_launch",
+    "tsl_engine_verify_wait", "tsl_engine_dj", "tsl_validate",
     "tsl_engine_last_kernel_ms", "tsl_engine_last_root_ms", "tsl_counters", "tsl_sp_stats",
 )
 
@@ -134,6 +135,12 @@ def lib():
     L.tsl_counters.argtypes = [vp, vp, vp]
     L.tsl_engine_last_kernel_ms.restype = ctypes.c_float
     L.tsl_engine_last_kernel_ms.argtypes = [vp]
+    L.tsl_engine_verify_stash.restype = i32
+    L.tsl_engine_verify_stash.argtypes = [vp, i32, i64, vp]
+    L.tsl_engine_verify_launch.restype = i32
+    L.tsl_engine_verify_launch.argtypes = [vp, i32, i64, vp, vp, vp, vp, i64]
+    L.tsl_engine_verify_wait.restype = i32
+    L.tsl_engine_verify_wait.argtypes = [vp, i32, vp, vp, vp]
     L.tsl_validate.restype = i32
     L.tsl_validate.argtypes = [i32, i32, vp, vp, vp, i32, vp, i32, vp, vp, i64, i64, vp, vp, vp,
                                vp, vp, vp, vp]
@@ -350,6 +357,35 @@ class Engine:
             check(self._L.tsl_engine_verify(self._h, n, _ptr(w), _ptr(per), _ptr(bud),
                                             -1 if cap is None else int(cap), _ptr(st), _ptr(nd),
                                             _ptr(rows)))
+        return st[:n].copy(), nd[:n].copy(), rows[:n * self.K].reshape(n, self.K).copy()
+
+    def verify_stash(self, slot: int, widx):
+        """Keep the assignments of these window indices (row positions
+        0..len-1) for asynchronous verification in `slot`."""
+        w = np.ascontiguousarray(widx, dtype=np.int64)
+        check(self._L.tsl_engine_verify_stash(self._h, int(slot), int(w.size), _ptr(w)))
+
+    def verify_launch(self, slot: int, pos, widx, periods, budgets, cap):
+        """Start verifying (row position, widx, period, cap) in `slot`."""
+        self._vk = getattr(self, "_vk", {})
+        arrs = [np.ascontiguousarray(pos, dtype=np.int64),
+                np.ascontiguousarray(widx, dtype=np.int64),
+                np.ascontiguousarray(periods, dtype=np.int32),
+                np.ascontiguousarray(budgets, dtype=np.int64)]
+        self._vk[slot] = (arrs, int(arrs[0].size))
+        check(self._L.tsl_engine_verify_launch(self._h, int(slot), arrs[0].size, _ptr(arrs[0]),
+                                               _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]),
+                                               -1 if cap is None else int(cap)))
+
+    def verify_wait(self, slot: int):
+        """Results of the slot's launch -> (status[], nodes[], starts[count, K])."""
+        n = self._vk[slot][1]
+        st = np.zeros(max(n, 1), dtype=np.int32)
+        nd = np.zeros(max(n, 1), dtype=np.int64)
+        rows = np.zeros(max(n, 1) * self.K, dtype=np.int32)
+        if n:
+            check(self._L.tsl_engine_verify_wait(self._h, int(slot), _ptr(st), _ptr(nd),
+                                                 _ptr(rows)))
         return st[:n].copy(), nd[:n].copy(), rows[:n * self.K].reshape(n, self.K).copy()
 
     def dj(self, assignments, periods, cap, budget, mode=1):

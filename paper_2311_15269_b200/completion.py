@@ -12,6 +12,7 @@ and the lazy feasibility checks) runs its decide probes on the GPU too.
 from __future__ import annotations
 
 import bisect
+import os
 import time
 from collections.abc import Sequence
 from dataclasses import dataclass, field
@@ -304,6 +305,10 @@ class _Feasibility:
         return ok, sched
 
 
+# scan window w+1 while window w's pending probes are verified (engine.py)
+PIPELINE_WINDOWS = os.environ.get("TESSEL_PIPELINE_WINDOWS", "1") == "1"
+
+
 def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optional[int] = None,
            lazy: bool = True, budget: Optional[float] = None, jobs: int = 1,
            device: Optional[int] = None, engine: Optional[BatchedRepetendSearch] = None,
@@ -339,65 +344,132 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
     optimal = total + 1
     done = False
     t_rep = time.monotonic()
-    for n_r in range(1, max(limit, 1) + 1):
-        if done:
-            break
-        count = eng.count(n_r)
-        r0, width = 0, WINDOW_FIRST
-        while r0 < count and not done:
-            if time.monotonic() > deadline:
-                report.timed_out = True
-                done = True
+
+    def windows():
+        """(n_r, r0, r1) in the reference's candidate order, windows growing."""
+        for n_r in range(1, max(limit, 1) + 1):
+            count = eng.count(n_r)
+            r0, width = 0, WINDOW_FIRST
+            while r0 < count:
+                r1 = min(count, r0 + width)
+                yield n_r, r0, r1
+                r0 = r1
+                width = min(width * WINDOW_GROWTH, WINDOW_MAX)
+
+    def replay(n_r, r0, r1, a0, win) -> bool:
+        """Ordered replay of a window's first SATs (completion.py:351-382);
+        True = the search ends (load bound reached)."""
+        nonlocal best, best_completed, optimal
+        first_sat = {a0 - r0 + w: v for w, v in win.first_sat.items()}
+        if comm is not None:
+            merged: dict = {}
+            for part in comm.allgather(first_sat):
+                merged.update(part)
+            first_sat = merged
+        special: dict = {}
+        used = r1 - r0
+        stop = False
+        for widx in sorted(first_sat):
+            period, starts = first_sat[widx]
+            if period >= optimal:
+                continue  # first SAT beyond this candidate's bound: "bound"
+            a = eng.unrank(n_r, r0 + widx)
+            rep = make_repetend(p, a, [int(v) for v in starts], period)
+            ok, sched = feas.replay(rep, report)
+            status = "completion-infeasible"
+            if ok:
+                best, optimal = rep, rep.period
+                if not lazy:
+                    best_completed = sched
+                report.improvements.append((a, optimal))
+                status = "improved"
+            special[widx] = CandidateRecord(n_r, a, rep.period, status)
+            if ok and optimal == lb:
+                stop = True
+                used = widx + 1
                 break
-            r1 = min(count, r0 + width)
-            if comm is not None:  # rank-prefix shard of the window (parallel.py)
-                a0, b0 = split_range(r0, r1, comm.rank, comm.size)
-                win = eng.evaluate_window(n_r, a0, b0, cap, optimal, feasible, 0.0,
-                                          LevelSync(comm, a0 - r0))
-            else:
-                a0 = r0
-                win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
-            if win.timed_out:
-                report.timed_out = True
-                done = True
-                break
-            first_sat = {a0 - r0 + w: v for w, v in win.first_sat.items()}
+        infeasible = 0
+        if win.gate is not None:
+            mine = max(0, min(win.count, r0 + used - a0))
+            infeasible = int(mine - win.gate[:mine].sum())
             if comm is not None:
-                merged: dict = {}
-                for part in comm.allgather(first_sat):
-                    merged.update(part)
-                first_sat = merged
-            # ordered replay (completion.py:351-382)
-            special: dict = {}
-            used = r1 - r0
-            for widx in sorted(first_sat):
-                period, starts = first_sat[widx]
-                if period >= optimal:
-                    continue  # first SAT beyond this candidate's bound: "bound"
-                a = eng.unrank(n_r, r0 + widx)
-                rep = make_repetend(p, a, [int(v) for v in starts], period)
-                ok, sched = feas.replay(rep, report)
-                status = "completion-infeasible"
-                if ok:
-                    best, optimal = rep, rep.period
-                    if not lazy:
-                        best_completed = sched
-                    report.improvements.append((a, optimal))
-                    status = "improved"
-                special[widx] = CandidateRecord(n_r, a, rep.period, status)
-                if ok and optimal == lb:
-                    done = True
-                    used = widx + 1
+                infeasible = comm.allreduce_sum([infeasible])[0]
+        log.add_segment(n_r, r0, used, special, infeasible)
+        return stop
+
+    def predicted_optimal(n_r, r0, win) -> int:
+        """The bound after replaying `win` if its speculation holds: the
+        replay rule run without side effects (memoised completion checks)."""
+        opt = optimal
+        for widx in sorted(win.first_sat):
+            period, starts = win.first_sat[widx]
+            if period >= opt:
+                continue
+            rep = make_repetend(p, eng.unrank(n_r, r0 + widx), [int(v) for v in starts], period)
+            if feas.ok(rep):
+                opt = rep.period
+        return opt
+
+    pipelined = comm is None and PIPELINE_WINDOWS and hasattr(eng, "begin_window")
+    inflight = None  # (n_r, r0, r1, job): scanned, its pending probes being verified
+    slot = 0
+    for n_r, r0, r1 in windows():
+        if time.monotonic() > deadline:
+            report.timed_out = True
+            done = True
+            break
+        if comm is not None:  # rank-prefix shard of the window (parallel.py)
+            a0, b0 = split_range(r0, r1, comm.rank, comm.size)
+            win = eng.evaluate_window(n_r, a0, b0, cap, optimal, feasible, 0.0,
+                                      LevelSync(comm, a0 - r0))
+        elif not pipelined:
+            a0 = r0
+            win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
+        else:
+            # Scan this window while the previous window's pending probes are
+            # verified, under the bound the previous window's replay yields if
+            # its speculation holds (else the true bound is lower: the scan
+            # only did extra work); then settle and replay in order.
+            a0 = r0
+            bound = optimal
+            if inflight is not None:
+                pn, p0, p1, pjob = inflight
+                bound = predicted_optimal(pn, p0, pjob.res)
+            job = eng.begin_window(n_r, r0, r1, cap, bound, feasible, deadline, slot)
+            slot ^= 1
+            if inflight is not None:
+                pwin = eng.finish_window(pjob, feasible)
+                inflight = None
+                if pwin.timed_out:
+                    report.timed_out = done = True
                     break
-            infeasible = 0
-            if win.gate is not None:
-                mine = max(0, min(win.count, r0 + used - a0))
-                infeasible = int(mine - win.gate[:mine].sum())
-                if comm is not None:
-                    infeasible = comm.allreduce_sum([infeasible])[0]
-            log.add_segment(n_r, r0, used, special, infeasible)
-            r0 = r1
-            width = min(width * WINDOW_GROWTH, WINDOW_MAX)
+                if replay(pn, p0, p1, p0, pwin):
+                    done = True
+                    break
+                if optimal > bound:
+                    # a repaired / rescanned misprediction left a higher bound
+                    # than predicted: this window missed periods — redo it
+                    win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
+                    job = None
+            if job is not None and job.launched:
+                inflight = (n_r, r0, r1, job)
+                continue
+            if job is not None:
+                win = eng.finish_window(job, feasible)  # nothing to verify: settle now
+        if win.timed_out:
+            report.timed_out = True
+            done = True
+            break
+        if replay(n_r, r0, r1, a0, win):
+            done = True
+            break
+    if inflight is not None and not done:
+        pn, p0, p1, pjob = inflight
+        pwin = eng.finish_window(pjob, feasible)
+        if pwin.timed_out:
+            report.timed_out = True
+        else:
+            replay(pn, p0, p1, p0, pwin)
     report.phase_secs["repetend"] += time.monotonic() - t_rep
     c = eng.counters
     report.engine = dict(c.__dict__)

@@ -683,7 +683,9 @@ __global__ void __launch_bounds__(128) k_verify_warp(const int *__restrict__ gpo
                                                      const long long *__restrict__ vbudget,
                                                      int count, int cap, int *vstatus,
                                                      long long *vnodes, int *vstarts,
-                                                     int *vlim, int pmin, int nlev) {
+                                                     int *vlim, int pmin, int nlev,
+                                                     const unsigned char *__restrict__ rows,
+                                                     const int *__restrict__ vpos) {
   extern __shared__ int sp[];
   load_pool(sp, gpool);
   const int K = sp[R_K];
@@ -711,7 +713,9 @@ __global__ void __launch_bounds__(128) k_verify_warp(const int *__restrict__ gpo
       }
       continue;
     }
-    const unsigned char *a = assign + (long long)widx * K;
+    // rows: the window's assignments stashed privately (the staged window
+    // may already hold the next one); else the staged window
+    const unsigned char *a = rows ? rows + (long long)vpos[t] * K : assign + (long long)widx * K;
     if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
     __syncwarp();
     const RepView v = rep_view(sp, P, cap, deplag, init);
@@ -777,6 +781,14 @@ __global__ void __launch_bounds__(128) k_dj_batch(const int *__restrict__ gpool,
     }
     __syncwarp();
   }
+}
+
+__global__ void k_stash_rows(const unsigned char *__restrict__ assign,
+                             const int *__restrict__ widx, int count, int K,
+                             unsigned char *__restrict__ rows) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)count * K) return;
+  rows[t] = assign[(long long)widx[t / K] * K + t % K];
 }
 
 __global__ void k_gather_rows(const int *__restrict__ rows, const int *__restrict__ pos, int count,
@@ -1131,6 +1143,20 @@ struct tsl_engine {
   size_t d_gather_cap = 0;
   char *d_verify = nullptr;
   size_t d_verify_cap = 0;
+  // asynchronous verification slots (windows in flight while the next one
+  // is scanned): private assignment rows + their own buffers and stream
+  struct VSlot {
+    unsigned char *rows = nullptr;
+    size_t rows_cap = 0;
+    long long n_rows = 0;
+    char *buf = nullptr;
+    size_t cap = 0;
+    long long count = 0;
+    int *d_st = nullptr, *d_s = nullptr;
+    long long *d_n = nullptr;
+    cudaEvent_t ev_go = nullptr, ev0 = nullptr, ev1 = nullptr;
+  } vslot[2];
+  cudaStream_t vstream = nullptr;
   // per-thread DFS scratch
   int *d_ws = nullptr;
   long long ws_words = 0;
@@ -1152,6 +1178,12 @@ struct tsl_engine {
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
     CK(cudaEventCreate(&evm));
+    CK(cudaStreamCreateWithFlags(&vstream, cudaStreamNonBlocking));
+    for (auto &vs : vslot) {
+      CK(cudaEventCreateWithFlags(&vs.ev_go, cudaEventDisableTiming));
+      CK(cudaEventCreate(&vs.ev0));
+      CK(cudaEventCreate(&vs.ev1));
+    }
     CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaMalloc(&d_pool, pool.size() * sizeof(int)));
     h2d(d_pool, pool.data(), pool.size() * sizeof(int), stream);
@@ -1225,6 +1257,14 @@ struct tsl_engine {
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     cudaEventDestroy(evm);
+    for (auto &vs : vslot) {
+      if (vs.rows) cudaFree(vs.rows);
+      if (vs.buf) cudaFree(vs.buf);
+      cudaEventDestroy(vs.ev_go);
+      cudaEventDestroy(vs.ev0);
+      cudaEventDestroy(vs.ev1);
+    }
+    cudaStreamDestroy(vstream);
     cudaStreamDestroy(stream);
   }
 };
@@ -1716,7 +1756,8 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
   COUNT_LAUNCH();
   k_verify_warp<<<(int)blocks, 32 * wpb, smem, e->stream>>>(e->d_pool, e->d_assign, d_w, d_p,
                                                              d_b, (int)count, icap, d_st, d_n,
-                                                             d_s, d_lim, pmin, nlev);
+                                                             d_s, d_lim, pmin, nlev, nullptr,
+                                                             nullptr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e->ev1, e->stream));
   d2h(status_out, d_st, count * sizeof(int), e->stream);
@@ -1724,6 +1765,130 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
   d2h(starts_out, d_s, (size_t)count * K * sizeof(int), e->stream);
   CK(cudaStreamSynchronize(e->stream));
   CK(cudaEventElapsedTime(&e->last_ms, e->ev0, e->ev1));
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_verify_stash(tsl_engine *e, int slot, int64_t count, const int64_t *widx) {
+  API_BEGIN
+  if (!e->gpu_ready) throw tsl::Error(TSL_EINVAL, "verify_stash before tsl_engine_stage");
+  if (slot < 0 || slot > 1) throw tsl::Error(TSL_EINVAL, "verify slot must be 0 or 1");
+  CK(cudaSetDevice(e->device));
+  auto &vs = e->vslot[slot];
+  CK(cudaStreamSynchronize(e->vstream));  // the slot's previous work is done
+  const int K = e->pool[R_K];
+  const size_t need = (size_t)std::max<int64_t>(count, 1) * K;
+  if (need > vs.rows_cap) {
+    if (vs.rows) CK(cudaFree(vs.rows));
+    CK(cudaMalloc(&vs.rows, need));
+    vs.rows_cap = need;
+  }
+  vs.n_rows = count;
+  if (count > 0) {
+    std::vector<int> w32(count);
+    for (long long i = 0; i < count; ++i) {
+      if (widx[i] < 0 || widx[i] >= e->W) throw tsl::Error(TSL_EINVAL, "stash: bad window index");
+      w32[i] = (int)widx[i];
+    }
+    int *d_w = nullptr;
+    CK(cudaMalloc(&d_w, count * sizeof(int)));
+    DevFree guard;
+    guard.add(d_w);
+    h2d(d_w, w32.data(), count * sizeof(int), e->stream);
+    const long long total = count * K;
+    COUNT_LAUNCH();
+    k_stash_rows<<<(int)((total + 255) / 256), 256, 0, e->stream>>>(e->d_assign, d_w,
+                                                                     (int)count, K, vs.rows);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(e->stream));
+  }
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64_t *pos,
+                             const int64_t *widx, const int32_t *period,
+                             const int64_t *node_budget, int64_t cap) {
+  API_BEGIN
+  if (slot < 0 || slot > 1) throw tsl::Error(TSL_EINVAL, "verify slot must be 0 or 1");
+  auto &vs = e->vslot[slot];
+  vs.count = count;
+  if (count <= 0) return TSL_OK;
+  CK(cudaSetDevice(e->device));
+  const int K = e->pool[R_K];
+  const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
+  std::vector<int> w32(count), p32(count), s32(count);
+  int pmin = period[0], pmax = period[0];
+  for (long long i = 0; i < count; ++i) {
+    if (pos[i] < 0 || pos[i] >= vs.n_rows) throw tsl::Error(TSL_EINVAL, "verify: bad row position");
+    tsl::ck(2LL * (K - 1) * ((long long)period[i] + e->pool[R_MAXDUR]) + 4LL * e->pool[R_TOTAL],
+            "period anchor");
+    w32[i] = (int)widx[i];
+    p32[i] = period[i];
+    s32[i] = (int)pos[i];
+    pmin = std::min(pmin, period[i]);
+    pmax = std::max(pmax, period[i]);
+  }
+  const int nlev = pmax - pmin + 1;
+  const size_t b_i = ((size_t)count * sizeof(int) + 255) / 256 * 256;
+  const size_t b_l = ((size_t)count * sizeof(long long) + 255) / 256 * 256;
+  const size_t b_lim = ((size_t)nlev * sizeof(int) + 255) / 256 * 256;
+  const size_t need = 4 * b_i + 2 * b_l + b_lim + (size_t)count * K * sizeof(int);
+  CK(cudaStreamSynchronize(e->vstream));
+  if (need > vs.cap) {
+    if (vs.buf) CK(cudaFree(vs.buf));
+    CK(cudaMalloc(&vs.buf, need));
+    vs.cap = need;
+  }
+  char *q = vs.buf;
+  int *d_w = (int *)q; q += b_i;
+  int *d_p = (int *)q; q += b_i;
+  int *d_pos = (int *)q; q += b_i;
+  vs.d_st = (int *)q; q += b_i;
+  long long *d_b = (long long *)q; q += b_l;
+  vs.d_n = (long long *)q; q += b_l;
+  int *d_lim = (int *)q; q += b_lim;
+  vs.d_s = (int *)q;
+  std::vector<int> lim0(nlev, 0x7fffffff);
+  // uploads on the verification stream (synchronous w.r.t. the host buffers)
+  h2d(d_lim, lim0.data(), nlev * sizeof(int), e->vstream);
+  h2d(d_w, w32.data(), count * sizeof(int), e->vstream);
+  h2d(d_p, p32.data(), count * sizeof(int), e->vstream);
+  h2d(d_pos, s32.data(), count * sizeof(int), e->vstream);
+  h2d(d_b, node_budget, count * sizeof(long long), e->vstream);
+  CK(cudaStreamSynchronize(e->vstream));
+  const int wpb = 4;
+  const size_t smem = (size_t)(((e->pool.size() + 3) & ~(size_t)3) +
+                               wpb * ((rep_warp_smem_words(e->pool.data()) + 3) & ~3)) *
+                      sizeof(int);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_verify_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  long long blocks = std::min<long long>((count + wpb - 1) / wpb, (long long)e->num_sms * 16);
+  CK(cudaEventRecord(vs.ev0, e->vstream));
+  COUNT_LAUNCH();
+  k_verify_warp<<<(int)blocks, 32 * wpb, smem, e->vstream>>>(
+      e->d_pool, e->d_assign, d_w, d_p, d_b, (int)count, icap, vs.d_st, vs.d_n, vs.d_s, d_lim,
+      pmin, nlev, vs.rows, d_pos);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(vs.ev1, e->vstream));
+  return TSL_OK;
+  API_END
+}
+
+int tsl_engine_verify_wait(tsl_engine *e, int slot, int32_t *status_out, int64_t *nodes_out,
+                           int32_t *starts_out) {
+  API_BEGIN
+  if (slot < 0 || slot > 1) throw tsl::Error(TSL_EINVAL, "verify slot must be 0 or 1");
+  auto &vs = e->vslot[slot];
+  if (vs.count <= 0) return TSL_OK;
+  CK(cudaSetDevice(e->device));
+  const int K = e->pool[R_K];
+  d2h(status_out, vs.d_st, vs.count * sizeof(int), e->vstream);
+  d2h(nodes_out, vs.d_n, vs.count * sizeof(long long), e->vstream);
+  d2h(starts_out, vs.d_s, (size_t)vs.count * K * sizeof(int), e->vstream);
+  CK(cudaStreamSynchronize(e->vstream));
+  CK(cudaEventElapsedTime(&e->last_ms, vs.ev0, vs.ev1));
   return TSL_OK;
   API_END
 }

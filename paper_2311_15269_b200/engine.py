@@ -112,6 +112,16 @@ class EngineCounters:
 
 
 @dataclass
+class WindowJob:
+    """A scanned window whose pending probes are being verified."""
+    args: tuple
+    res: "WindowResult"
+    pending: list
+    slot: int
+    launched: bool
+
+
+@dataclass
 class WindowResult:
     n_r: int
     r0: int
@@ -181,9 +191,68 @@ class BatchedRepetendSearch:
     def close(self):
         self.eng.close()
 
+    # ---- pipelined windows: scan window w+1 while window w is verified ----
+    def begin_window(self, n_r: int, r0: int, r1: int, cap: Optional[int], bound: int,
+                     feasible, deadline: float = 0.0, slot: int = 0) -> "WindowJob":
+        """Scan a window and launch the verification of its pending probes
+        asynchronously (its assignments stashed in `slot`), so that the next
+        window can be staged and scanned meanwhile.  The scan may run under a
+        stale (higher) bound than the exact sequential one: its outcomes are
+        facts about (candidate, period) pairs and the ordered replay applies
+        the true bound, so only work is added, never a different answer."""
+        res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, None, {})
+        job = WindowJob((n_r, r0, r1, cap, bound, deadline), res, pending, slot, False)
+        if pending and not res.timed_out:
+            self.eng.verify_stash(slot, [x for x, _ in pending])
+            self._launch_round(job, list(range(len(pending))))
+            job.launched = True
+        return job
+
+    def _launch_round(self, job, positions):
+        n_r, r0, r1, cap, bound, deadline = job.args
+        w = [job.pending[i][0] for i in positions]
+        per = [job.pending[i][1] for i in positions]
+        bud = [0 if q == self.lb else PROBE_NODES for q in per]
+        run_bud = [VERIFY_FIRST if (b == 0 or b > VERIFY_FIRST) else b for b in bud]
+        self.eng.verify_launch(job.slot, positions, w, per, run_bud, cap)
+
+    def finish_window(self, job: "WindowJob", feasible) -> WindowResult:
+        n_r, r0, r1, cap, bound, deadline = job.args
+        if job.res.timed_out:
+            return job.res
+        hints: dict = {}
+        first = self.eng.verify_wait(job.slot) if job.launched else None
+        index = {xq: i for i, xq in enumerate(job.pending)}
+
+        def run(todo, w, per, run_bud):
+            self._launch_round(job, [index[xq] for xq in todo])
+            return self.eng.verify_wait(job.slot)
+
+        sats = self._verify_pending(n_r, r0, cap, job.pending, feasible, hints, first=first,
+                                    runner=run)
+        res = job.res
+        fix = self._first_sats(sats)
+        if not fix:
+            return res
+        if not (set(fix) & res.retirers) and self.repair:
+            for x, (q, row) in fix.items():
+                res.first_sat[x] = (q, row)
+            self.counters.repaired += len(fix)
+            return res
+        self.counters.redo += 1  # rescan (the window is staged again) with the hints
+        return self.evaluate_window(n_r, r0, r1, cap, bound, feasible, deadline, None, hints)
+
+    @staticmethod
+    def _first_sats(sats) -> dict:
+        fix: dict = {}
+        for x, q, row in sats:
+            if x not in fix or q < fix[x][0]:
+                fix[x] = (q, row)
+        return fix
+
     def evaluate_window(self, n_r: int, r0: int, r1: int, cap: Optional[int], bound: int,
                         feasible: Callable[[int, int, int, np.ndarray], bool],
-                        deadline: float = 0.0, sync=None) -> WindowResult:
+                        deadline: float = 0.0, sync=None, hints=None) -> WindowResult:
         """Level-synchronous period scan of ranks [r0, r1) at n_r under the
         sequential bound ``bound`` in force at the window start.
         ``feasible(n_r, rank, period, starts)`` is the completion check.
@@ -204,7 +273,7 @@ class BatchedRepetendSearch:
         retired at P only carry first SATs at periods >= P, which the ordered
         replay skips once w's period is the bound.  Otherwise the window is
         scanned again with every verified outcome as a hint."""
-        hints: dict = {}
+        hints = {} if hints is None else hints
         for _ in range(1 + 4 * 64):
             res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, sync,
                                              hints)
@@ -229,7 +298,7 @@ class BatchedRepetendSearch:
             self.counters.redo += 1
         raise RuntimeError("speculation did not converge")
 
-    def _verify_pending(self, n_r, r0, cap, pending, feasible, hints):
+    def _verify_pending(self, n_r, r0, cap, pending, feasible, hints, first=None, runner=None):
         """Settle the window's pending (speculated) probes in concurrent
         launches.  The kernel lets a SAT (x, q) cancel pairs (x2, q2) with
         x2 > x and q2 >= q; a cancelled pair is re-run unless such a SAT
@@ -250,7 +319,13 @@ class BatchedRepetendSearch:
             # VERIFY_FIRST nodes; longer ones run one at a time through the
             # subtree-parallel decide (sp_dfs.cuh) below
             run_bud = [VERIFY_FIRST if (b == 0 or b > VERIFY_FIRST) else b for b in bud]
-            st, nodes, rows = self.eng.verify(w, per, run_bud, cap)
+            if first is not None:  # round 1 already ran asynchronously (begin_window)
+                st, nodes, rows = first
+                first = None
+            elif runner is not None:
+                st, nodes, rows = runner(todo, w, per, run_bud)
+            else:
+                st, nodes, rows = self.eng.verify(w, per, run_bud, cap)
             self.counters.add({"probes": 0, "root_refuted": 0, "nodes": int(nodes.sum()),
                                "capped": int((st == _native.TIMEOUT).sum()),
                                "sat": int((st == _native.SAT).sum()), "deferred": 0,

@@ -152,6 +152,33 @@ class OracleEngine:
         return (np.array(st, dtype=np.int32), np.array(nodes, dtype=np.int64),
                 np.array(rows, dtype=np.int32).reshape(len(st), self.K))
 
+    def verify_stash(self, slot, widx):
+        self._stash = getattr(self, "_stash", {})
+        self._stash[slot] = [self.cands[int(w)] for w in widx]
+
+    def verify_launch(self, slot, pos, widx, periods, budgets, cap):
+        # computed now, read at verify_wait (the device runs it meanwhile);
+        # the stashed assignments, not the staged window, are probed
+        saved, cancel = self.cands, self.cancel
+        rows = self._stash[slot]
+        self.cands, self.cancel = [rows[int(p)] for p in pos], False
+        try:
+            out = self.verify(list(range(len(pos))), periods, budgets, cap)
+        finally:
+            self.cands, self.cancel = saved, cancel
+        st = out[0]
+        if self.cancel:  # cancellation compares window indices, not positions
+            sats = [(int(w), int(q)) for w, q, s in zip(widx, periods, st) if s == oracle.SAT]
+            st = st.copy()
+            for i, (w, q) in enumerate(zip(widx, periods)):
+                if any(x < int(w) and p <= int(q) for x, p in sats):
+                    st[i] = 3
+        self._vres = getattr(self, "_vres", {})
+        self._vres[slot] = (st, out[1], out[2])
+
+    def verify_wait(self, slot):
+        return self._vres[slot]
+
     def sat_rows(self, first, count):
         self.sats.sort(key=lambda r: r[0])
         part = self.sats[first:first + count]
