@@ -49,6 +49,23 @@ inline std::vector<int> dup_flags(const std::vector<int> &ptr, const std::vector
   return out;
 }
 
+// per in-list entry p of node a: the position (within a's out-list) of the
+// out-entry naming the same node, or -1 — the warp propagation's one-chunk
+// path (wrx_dfs.cuh) deduplicates a node on both lists with it
+inline std::vector<int> in_twins(const std::vector<int> &out_ptr, const std::vector<int> &out_dst,
+                                 const std::vector<int> &in_ptr, const std::vector<int> &in_src,
+                                 int n) {
+  std::vector<int> tw(in_src.empty() ? 1 : in_src.size(), -1);
+  for (int a = 0; a < n; ++a)
+    for (int p = in_ptr[a]; p < in_ptr[a + 1]; ++p)
+      for (int q = out_ptr[a]; q < out_ptr[a + 1]; ++q)
+        if (out_dst[q] == in_src[p]) {
+          tw[p] = q - out_ptr[a];
+          break;
+        }
+  return tw;
+}
+
 // ------------------------------------------------------------------ GenView
 inline std::vector<int> gen_build(int n, const int64_t *dur, const uint64_t *devmask,
                                   const int64_t *mem, const int64_t *edges, int m,
@@ -155,6 +172,7 @@ inline std::vector<int> gen_build(int n, const int64_t *dur, const uint64_t *dev
   put(devof);
   put(dup_flags(out_ptr, out_dst, n));
   put(dup_flags(in_ptr, in_src, n));
+  put(in_twins(out_ptr, out_dst, in_ptr, in_src, n));
   pool[G_WORDS] = (int)pool.size();
   return pool;
 }
@@ -354,6 +372,7 @@ inline std::vector<int> rep_build(const Placement &pl) {
   put(R_FR, fr);
   put(R_DPPTR, dp_ptr);
   put(R_DP, dp);
+  put(R_INTWIN, in_twins(out_ptr, out_dst, in_ptr, in_src, K));
   pool[R_WORDS] = (int)pool.size();
   // value-range guard for the int32 device arithmetic: anchors reach
   // 2 (K-1)(P + max t) with P <= total.

@@ -21,9 +21,11 @@ struct GenView {
   const int *out_ptr_, *out_dst_, *out_lag_, *in_ptr_, *in_src_, *in_lag_;
   const int *conf_ptr_, *conf_dst_, *dev_ptr_, *dev_items_, *devof_ptr_, *devof_;
   const int *out_dup_, *in_dup_;  // 1 if the node's edge list repeats a target
+  const int *in_twin_;            // host_build.hpp in_twins
 
   RX_HD int n() const { return n_; }
   RX_HD bool out_dup(int a) const { return out_dup_[a] != 0; }
+  RX_HD int in_twin(int p) const { return in_twin_[p]; }
   RX_HD bool in_dup(int a) const { return in_dup_[a] != 0; }
   RX_HD int ndev() const { return ndev_; }
   RX_HD int cap() const { return cap_; }
@@ -84,7 +86,8 @@ RX_HD GenView gen_view(const int *pool) {
   g.devof_ptr_ = p; p += n + 1;
   g.devof_ = p; p += nmemb;
   g.out_dup_ = p; p += n;
-  g.in_dup_ = p;
+  g.in_dup_ = p; p += n;
+  g.in_twin_ = p;
   return g;
 }
 
@@ -105,6 +108,8 @@ enum {
   R_LSPTR, R_LS, R_HSPTR, R_HS, R_FRPTR, R_FR,
   // device -> disjunctive pairs on it (warp disjunctive filter)
   R_DPPTR, R_DP,
+  // per in-entry: position of the out-entry naming the same node, or -1
+  R_INTWIN,
   R_WORDS, R_HDR
 };
 
@@ -117,7 +122,7 @@ struct RepView {
   const int *dur_, *mem_, *order_, *out_ptr_, *out_dst_, *out_row_, *out_dep_end_;
   const int *in_ptr_, *in_src_, *in_row_, *in_dep_end_, *in_srcdur_;
   const int *conf_ptr_, *conf_dst_, *dev_ptr_, *dev_items_, *devof_ptr_, *devof_;
-  const int *out_dup_, *in_dup_;
+  const int *out_dup_, *in_dup_, *in_twin_;
   const int *deplag;  // per dependency row: base - (a[src] - a[dst]) * P
   const int *init;    // entry memory per device
   int K, D, P, cap_;
@@ -125,6 +130,7 @@ struct RepView {
   RX_HD int n() const { return K; }
   RX_HD int ndev() const { return D; }
   RX_HD bool out_dup(int a) const { return out_dup_[a] != 0; }
+  RX_HD int in_twin(int p) const { return in_twin_[p]; }
   RX_HD bool in_dup(int a) const { return in_dup_[a] != 0; }
   RX_HD int cap() const { return cap_; }
   RX_HD int dur(int i) const { return dur_[i]; }
@@ -182,6 +188,7 @@ RX_HD RepView rep_view(const int *pool, int P, int cap, const int *deplag, const
   v.devof_ = pool + pool[R_DEVOF];
   v.out_dup_ = pool + pool[R_OUTDUP];
   v.in_dup_ = pool + pool[R_INDUP];
+  v.in_twin_ = pool + pool[R_INTWIN];
   return v;
 }
 

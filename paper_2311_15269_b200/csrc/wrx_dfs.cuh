@@ -104,6 +104,56 @@ __device__ bool wrx_propagate(const M &md, WWs &w, int &qh, int &qt, int &qc) {
     if (lane == 0) atomicAnd(&w.inq[a >> 5], ~(1u << (a & 31)));
     __syncwarp();
     const int la = w.lo[a], ha = w.hi[a];
+    const int ob = md.out_begin(a), no = md.out_end(a) - ob;
+    const int ib = md.in_begin(a), ni = md.in_end(a) - ib;
+    if (no + ni <= 32 && !md.out_dup(a) && !md.in_dup(a)) {
+      // one chunk: lanes [0, no) relax the out-edges, lanes [no, no + ni) the
+      // in-edges.  Out-edges only raise lo and in-edges only lower hi, so the
+      // sequential order is kept by (1) out failures (nl > hi[b]) against
+      // the entry hi, (2) the out updates applied, (3) in failures
+      // (nh < lo[b]) against the updated lo, (4) one enqueue in lane order
+      // (= out-edge order, then in-edge order).  Neither list repeats a node;
+      // a node on both lists (in_twin) is enqueued by its out-lane if that
+      // lane enqueues it — the sequential in-edge would then find it queued.
+      const bool is_out = lane < no, is_in = !is_out && lane < no + ni;
+      int b = 0, nv = 0, lob = 0, hib = 0, tw = -1;
+      bool inq = true;
+      if (is_out) {
+        const int p = ob + lane;
+        b = md.out_dst(p);
+        nv = la + (p < md.out_dep_end(a) ? md.out_dep_lag(p) : md.out_win_lag(a));
+        lob = w.lo[b];
+      } else if (is_in) {
+        const int p = ib + lane - no;
+        b = md.in_src(p);
+        nv = ha - (p < md.in_dep_end(a) ? md.in_dep_lag(p) : md.in_win_lag(p));
+        tw = md.in_twin(p);
+      }
+      if (is_out || is_in) {
+        hib = w.hi[b];
+        inq = wrx_bit(w.inq, b);
+      }
+      const unsigned failo = __ballot_sync(WRX_FULL, is_out && nv > hib);
+      const int fo = failo ? __ffs(failo) - 1 : 32;
+      const bool impo = is_out && lane < fo && nv > lob;
+      __syncwarp();
+      if (impo) atomicMax(&w.lo[b], nv);
+      if (failo) {
+        wrx_enqueue(w, impo && !inq, b, n, qt, qc, false);
+        return false;
+      }
+      const unsigned ocand = __ballot_sync(WRX_FULL, impo && !inq);
+      __syncwarp();  // the out updates visible to the in-lanes
+      if (is_in) lob = w.lo[b];
+      const unsigned faili = __ballot_sync(WRX_FULL, is_in && nv < lob);
+      const int fi = faili ? __ffs(faili) - 1 : 32;
+      const bool impi = is_in && lane < fi && nv < hib;
+      if (impi) atomicMin(&w.hi[b], nv);
+      const bool twin_q = tw >= 0 && ((ocand >> tw) & 1u);
+      wrx_enqueue(w, (impo || (impi && !twin_q)) && !inq, b, n, qt, qc, false);
+      if (faili) return false;
+      continue;
+    }
     // out-edges: lo[b] >= lo[a] + lag
     {
       const int pb = md.out_begin(a), pe = md.out_end(a), od = md.out_dep_end(a);

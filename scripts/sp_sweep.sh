@@ -1,9 +1,8 @@
-# SP-DFS knob sweep on the long completion probes (one GPU; timings only)
-set -x
+# SP-DFS knob sweep on long completion probes (one GPU; timings only)
 export TESSEL_BUDGET_SECS=1e9
 out=gpurun_out/sp_sweep.log
 : > $out
-for pr in "C2_8 0" "C3_12 0" "C3_12 1" "C4a_4 0"; do
+for pr in "C2_8 0" "C3_12 0" "to_x4_n4 0"; do
   for pause in 16384 65536 262144; do
     for tn in 65536 262144; do
       echo "pause=$pause task_nodes=$tn" >> $out
