@@ -343,6 +343,36 @@ __device__ bool wrx_mem_ok(const M &md, WWs &w, int d, int cap) {
   // small devices: the O(k^2) shared-memory form measured faster than a sort
   if (k > 8 && k <= 32) return wrx_mem_ok32(md, w, d, cap, pb, k, k <= 16 ? 16 : 32);
   const int lane = wrx_lane();
+  if (k <= 8) {
+    // all (i, j) pairs in registers: lane = 8 * (i mod 4) + j, rows i and
+    // i + 4 in two passes; run(i) = init + sum of delta_j over events j with
+    // time_j <= time_i (delta_j = 0 for non-events), reduced over the 8 lanes
+    // of a row by xor shuffles
+    const int j = lane & 7;
+    int tj = 0, dj = 0;
+    bool evj = false;
+    if (j < k) {
+      const int it = md.dev_item(pb + j);
+      const int m = md.mem(it);
+      const bool pl = wrx_bit(w.placed, it);
+      evj = pl || m < 0;
+      tj = pl ? w.s[it] : w.lo[it];
+      dj = evj ? m : 0;
+    }
+    bool bad = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = (lane >> 3) + 4 * h;
+      const int ti = __shfl_sync(WRX_FULL, tj, i);
+      const bool evi = __shfl_sync(WRX_FULL, evj, i);
+      int c = (j < k && tj <= ti) ? dj : 0;
+      c += __shfl_xor_sync(WRX_FULL, c, 1);
+      c += __shfl_xor_sync(WRX_FULL, c, 2);
+      c += __shfl_xor_sync(WRX_FULL, c, 4);
+      bad |= i < k && evi && init + c > cap;
+    }
+    return !__any_sync(WRX_FULL, bad);
+  }
   for (int i = lane; i < k; i += 32) {
     const int it = md.dev_item(pb + i);
     const int m = md.mem(it);

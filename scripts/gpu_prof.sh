@@ -1,2 +1,3 @@
 set -x
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_sp_tasks --launch-count 1 -o gpurun_out/ncu_sptasks -f python scripts/sp_probe.py to_x4_n4 0 > gpurun_out/ncu_sptasks.log 2>&1
+export TESSEL_BUDGET_SECS=1e9
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_verify_warp --launch-count 1 -o gpurun_out/ncu_verify_c39 -f python scripts/trace_search.py C3@9 > gpurun_out/ncu_verify.log 2>&1
