@@ -160,12 +160,13 @@ int tsl_engine_add_active(tsl_engine *e, int64_t count, const int64_t *widx);
  * a reference status); the caller re-runs them unless that SAT's completion
  * check passes. */
 /* Asynchronous verification (engine.py pipelines windows): stash the
- * assignments of `count` window indices of the staged window into slot 0/1
- * (rows = positions 0..count-1), launch the verification of (row position,
- * window index, period, cap) quadruples of that slot on the engine's
- * verification stream — it runs while the next window is staged and
- * scanned — and wait for / read its results (same meaning as
- * tsl_engine_verify). */
+ * assignments of `count` window indices of the staged window into slot
+ * 0..TSL_VERIFY_SLOTS-1 (rows = positions 0..count-1), launch the
+ * verification of (row position, window index, period, cap) quadruples of
+ * that slot on the slot's own stream — it runs while later windows are
+ * staged and scanned, concurrently with the other slots — and wait for /
+ * read its results (same meaning as tsl_engine_verify). */
+#define TSL_VERIFY_SLOTS 4
 int tsl_engine_verify_stash(tsl_engine *e, int slot, int64_t count, const int64_t *widx);
 int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64_t *pos,
                              const int64_t *widx, const int32_t *period,

@@ -13,12 +13,14 @@ from __future__ import annotations
 
 import bisect
 import os
+from collections import deque
 import time
 from collections.abc import Sequence
 from dataclasses import dataclass, field
 from typing import Optional
 
-from .engine import WINDOW_FIRST, WINDOW_GROWTH, WINDOW_MAX, BatchedRepetendSearch
+from .engine import (VERIFY_SLOTS, WINDOW_FIRST, WINDOW_GROWTH, WINDOW_MAX,
+                     BatchedRepetendSearch)
 from .parallel import LevelSync, split_range
 from .placement import BlockInstance, PlacementSpec
 from .repetend import (Repetend, RepetendOutcome, entry_memory, lower_bound, make_repetend,
@@ -307,6 +309,9 @@ class _Feasibility:
 
 # scan window w+1 while window w's pending probes are verified (engine.py)
 PIPELINE_WINDOWS = os.environ.get("TESSEL_PIPELINE_WINDOWS", "1") == "1"
+# windows whose pending probes may be under verification at once (one
+# verification slot each, plus the slot of the window being scanned)
+PIPELINE_DEPTH = max(1, min(int(os.environ.get("TESSEL_PIPELINE_DEPTH", "3")), VERIFY_SLOTS - 1))
 
 
 def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optional[int] = None,
@@ -397,10 +402,10 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
         log.add_segment(n_r, r0, used, special, infeasible)
         return stop
 
-    def predicted_optimal(n_r, r0, win) -> int:
-        """The bound after replaying `win` if its speculation holds: the
-        replay rule run without side effects (memoised completion checks)."""
-        opt = optimal
+    def predicted_optimal(n_r, r0, win, opt) -> int:
+        """The bound after replaying `win` from bound `opt` if its
+        speculation holds: the replay rule run without side effects
+        (memoised completion checks)."""
         for widx in sorted(win.first_sat):
             period, starts = win.first_sat[widx]
             if period >= opt:
@@ -411,8 +416,37 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
         return opt
 
     pipelined = comm is None and PIPELINE_WINDOWS and hasattr(eng, "begin_window")
-    inflight = None  # (n_r, r0, r1, job): scanned, its pending probes being verified
-    slot = 0
+    # windows scanned whose pending probes are being verified, oldest first:
+    # [n_r, r0, r1, job, bound the window was scanned under]
+    inflight: deque = deque()
+
+    def settle_head() -> bool:
+        """Finish and replay the oldest window in flight; True = the search
+        ends (load bound reached or out of time)."""
+        pn, p0, p1, pjob, _ = inflight.popleft()
+        pwin = eng.finish_window(pjob, feasible)
+        if pwin.timed_out:
+            report.timed_out = True
+            return True
+        return replay(pn, p0, p1, p0, pwin)
+
+    def redo_mispredicted() -> bool:
+        """The next window in flight was scanned under a predicted bound; a
+        true bound above it (a repaired / rescanned misprediction) means it
+        missed periods: redo it and every later one, in order, exactly."""
+        if not inflight or optimal <= inflight[0][4]:
+            return False
+        redo = list(inflight)
+        inflight.clear()  # their verification results are dropped
+        for rn, q0, q1, _, _ in redo:
+            win = eng.evaluate_window(rn, q0, q1, cap, optimal, feasible, deadline)
+            if win.timed_out:
+                report.timed_out = True
+                return True
+            if replay(rn, q0, q1, q0, win):
+                return True
+        return False
+
     for n_r, r0, r1 in windows():
         if time.monotonic() > deadline:
             report.timed_out = True
@@ -426,36 +460,27 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
             a0 = r0
             win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
         else:
-            # Scan this window while the previous window's pending probes are
-            # verified, under the bound the previous window's replay yields if
-            # its speculation holds (else the true bound is lower: the scan
-            # only did extra work); then settle and replay in order.
-            a0 = r0
+            # Scan this window while the pending probes of up to
+            # PIPELINE_DEPTH earlier windows are verified (one stream each),
+            # under the bound their replays yield if their speculation holds
+            # (else the true bound is lower: the scan only did extra work);
+            # windows are settled and replayed strictly in order.
             bound = optimal
-            if inflight is not None:
-                pn, p0, p1, pjob = inflight
-                bound = predicted_optimal(pn, p0, pjob.res)
+            for pn, p0, _, pjob, _ in inflight:
+                bound = predicted_optimal(pn, p0, pjob.res, bound)
+            busy = {e[3].slot for e in inflight}
+            slot = next(k for k in range(VERIFY_SLOTS) if k not in busy)
             job = eng.begin_window(n_r, r0, r1, cap, bound, feasible, deadline, slot)
-            slot ^= 1
-            if inflight is not None:
-                pwin = eng.finish_window(pjob, feasible)
-                inflight = None
-                if pwin.timed_out:
-                    report.timed_out = done = True
-                    break
-                if replay(pn, p0, p1, p0, pwin):
+            inflight.append([n_r, r0, r1, job, bound])
+            # settle the oldest while too many are in flight, and every head
+            # with nothing to verify (it settles without waiting)
+            while inflight and (len(inflight) > PIPELINE_DEPTH or not inflight[0][3].launched):
+                if settle_head() or redo_mispredicted():
                     done = True
                     break
-                if optimal > bound:
-                    # a repaired / rescanned misprediction left a higher bound
-                    # than predicted: this window missed periods — redo it
-                    win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
-                    job = None
-            if job is not None and job.launched:
-                inflight = (n_r, r0, r1, job)
-                continue
-            if job is not None:
-                win = eng.finish_window(job, feasible)  # nothing to verify: settle now
+            if done:
+                break
+            continue
         if win.timed_out:
             report.timed_out = True
             done = True
@@ -463,13 +488,9 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
         if replay(n_r, r0, r1, a0, win):
             done = True
             break
-    if inflight is not None and not done:
-        pn, p0, p1, pjob = inflight
-        pwin = eng.finish_window(pjob, feasible)
-        if pwin.timed_out:
-            report.timed_out = True
-        else:
-            replay(pn, p0, p1, p0, pwin)
+    while inflight and not done:
+        if settle_head() or redo_mispredicted():
+            break
     report.phase_secs["repetend"] += time.monotonic() - t_rep
     c = eng.counters
     report.engine = dict(c.__dict__)

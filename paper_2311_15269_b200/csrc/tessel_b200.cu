@@ -1155,8 +1155,8 @@ struct tsl_engine {
     int *d_st = nullptr, *d_s = nullptr;
     long long *d_n = nullptr;
     cudaEvent_t ev_go = nullptr, ev0 = nullptr, ev1 = nullptr;
-  } vslot[2];
-  cudaStream_t vstream = nullptr;
+    cudaStream_t st = nullptr;  // the slot's verification stream
+  } vslot[TSL_VERIFY_SLOTS];
   // per-thread DFS scratch
   int *d_ws = nullptr;
   long long ws_words = 0;
@@ -1178,8 +1178,8 @@ struct tsl_engine {
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
     CK(cudaEventCreate(&evm));
-    CK(cudaStreamCreateWithFlags(&vstream, cudaStreamNonBlocking));
     for (auto &vs : vslot) {
+      CK(cudaStreamCreateWithFlags(&vs.st, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&vs.ev_go, cudaEventDisableTiming));
       CK(cudaEventCreate(&vs.ev0));
       CK(cudaEventCreate(&vs.ev1));
@@ -1263,8 +1263,8 @@ struct tsl_engine {
       cudaEventDestroy(vs.ev_go);
       cudaEventDestroy(vs.ev0);
       cudaEventDestroy(vs.ev1);
+      cudaStreamDestroy(vs.st);
     }
-    cudaStreamDestroy(vstream);
     cudaStreamDestroy(stream);
   }
 };
@@ -1772,10 +1772,10 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
 int tsl_engine_verify_stash(tsl_engine *e, int slot, int64_t count, const int64_t *widx) {
   API_BEGIN
   if (!e->gpu_ready) throw tsl::Error(TSL_EINVAL, "verify_stash before tsl_engine_stage");
-  if (slot < 0 || slot > 1) throw tsl::Error(TSL_EINVAL, "verify slot must be 0 or 1");
+  if (slot < 0 || slot >= TSL_VERIFY_SLOTS) throw tsl::Error(TSL_EINVAL, "bad verify slot");
   CK(cudaSetDevice(e->device));
   auto &vs = e->vslot[slot];
-  CK(cudaStreamSynchronize(e->vstream));  // the slot's previous work is done
+  CK(cudaStreamSynchronize(vs.st));  // the slot's previous work is done
   const int K = e->pool[R_K];
   const size_t need = (size_t)std::max<int64_t>(count, 1) * K;
   if (need > vs.rows_cap) {
@@ -1810,7 +1810,7 @@ int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64
                              const int64_t *widx, const int32_t *period,
                              const int64_t *node_budget, int64_t cap) {
   API_BEGIN
-  if (slot < 0 || slot > 1) throw tsl::Error(TSL_EINVAL, "verify slot must be 0 or 1");
+  if (slot < 0 || slot >= TSL_VERIFY_SLOTS) throw tsl::Error(TSL_EINVAL, "bad verify slot");
   auto &vs = e->vslot[slot];
   vs.count = count;
   if (count <= 0) return TSL_OK;
@@ -1834,7 +1834,7 @@ int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64
   const size_t b_l = ((size_t)count * sizeof(long long) + 255) / 256 * 256;
   const size_t b_lim = ((size_t)nlev * sizeof(int) + 255) / 256 * 256;
   const size_t need = 4 * b_i + 2 * b_l + b_lim + (size_t)count * K * sizeof(int);
-  CK(cudaStreamSynchronize(e->vstream));
+  CK(cudaStreamSynchronize(vs.st));
   if (need > vs.cap) {
     if (vs.buf) CK(cudaFree(vs.buf));
     CK(cudaMalloc(&vs.buf, need));
@@ -1851,12 +1851,12 @@ int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64
   vs.d_s = (int *)q;
   std::vector<int> lim0(nlev, 0x7fffffff);
   // uploads on the verification stream (synchronous w.r.t. the host buffers)
-  h2d(d_lim, lim0.data(), nlev * sizeof(int), e->vstream);
-  h2d(d_w, w32.data(), count * sizeof(int), e->vstream);
-  h2d(d_p, p32.data(), count * sizeof(int), e->vstream);
-  h2d(d_pos, s32.data(), count * sizeof(int), e->vstream);
-  h2d(d_b, node_budget, count * sizeof(long long), e->vstream);
-  CK(cudaStreamSynchronize(e->vstream));
+  h2d(d_lim, lim0.data(), nlev * sizeof(int), vs.st);
+  h2d(d_w, w32.data(), count * sizeof(int), vs.st);
+  h2d(d_p, p32.data(), count * sizeof(int), vs.st);
+  h2d(d_pos, s32.data(), count * sizeof(int), vs.st);
+  h2d(d_b, node_budget, count * sizeof(long long), vs.st);
+  CK(cudaStreamSynchronize(vs.st));
   const int wpb = 4;
   const size_t smem = (size_t)(((e->pool.size() + 3) & ~(size_t)3) +
                                wpb * ((rep_warp_smem_words(e->pool.data()) + 3) & ~3)) *
@@ -1865,13 +1865,13 @@ int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64
     CK(cudaFuncSetAttribute(k_verify_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
   long long blocks = std::min<long long>((count + wpb - 1) / wpb, (long long)e->num_sms * 16);
-  CK(cudaEventRecord(vs.ev0, e->vstream));
+  CK(cudaEventRecord(vs.ev0, vs.st));
   COUNT_LAUNCH();
-  k_verify_warp<<<(int)blocks, 32 * wpb, smem, e->vstream>>>(
+  k_verify_warp<<<(int)blocks, 32 * wpb, smem, vs.st>>>(
       e->d_pool, e->d_assign, d_w, d_p, d_b, (int)count, icap, vs.d_st, vs.d_n, vs.d_s, d_lim,
       pmin, nlev, vs.rows, d_pos);
   CK(cudaGetLastError());
-  CK(cudaEventRecord(vs.ev1, e->vstream));
+  CK(cudaEventRecord(vs.ev1, vs.st));
   return TSL_OK;
   API_END
 }
@@ -1879,15 +1879,15 @@ int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64
 int tsl_engine_verify_wait(tsl_engine *e, int slot, int32_t *status_out, int64_t *nodes_out,
                            int32_t *starts_out) {
   API_BEGIN
-  if (slot < 0 || slot > 1) throw tsl::Error(TSL_EINVAL, "verify slot must be 0 or 1");
+  if (slot < 0 || slot >= TSL_VERIFY_SLOTS) throw tsl::Error(TSL_EINVAL, "bad verify slot");
   auto &vs = e->vslot[slot];
   if (vs.count <= 0) return TSL_OK;
   CK(cudaSetDevice(e->device));
   const int K = e->pool[R_K];
-  d2h(status_out, vs.d_st, vs.count * sizeof(int), e->vstream);
-  d2h(nodes_out, vs.d_n, vs.count * sizeof(long long), e->vstream);
-  d2h(starts_out, vs.d_s, (size_t)vs.count * K * sizeof(int), e->vstream);
-  CK(cudaStreamSynchronize(e->vstream));
+  d2h(status_out, vs.d_st, vs.count * sizeof(int), vs.st);
+  d2h(nodes_out, vs.d_n, vs.count * sizeof(long long), vs.st);
+  d2h(starts_out, vs.d_s, (size_t)vs.count * K * sizeof(int), vs.st);
+  CK(cudaStreamSynchronize(vs.st));
   CK(cudaEventElapsedTime(&e->last_ms, vs.ev0, vs.ev1));
   return TSL_OK;
   API_END

@@ -78,14 +78,16 @@ def _expected(doc):
 @pytest.mark.parametrize("name", CASES)
 @pytest.mark.parametrize("small", [False, True])
 @pytest.mark.parametrize("speculate", [True, False])
-@pytest.mark.parametrize("pipeline", [True, False])
+@pytest.mark.parametrize("pipeline", [0, 1, 3])
 def test_level_scan_and_replay_match_reference(monkeypatch, name, small, speculate, pipeline):
     """Single shard: the GPU engine's host logic over the oracle stand-in,
-    with and without speculation of full-cap probes, with and without the
-    window pipeline (window w+1 scanned while window w is verified)."""
+    with and without speculation of full-cap probes, without the window
+    pipeline and with 1 or 3 earlier windows verified while a window is
+    scanned."""
     import paper_2311_15269_b200.completion as C
 
-    monkeypatch.setattr(C, "PIPELINE_WINDOWS", pipeline)
+    monkeypatch.setattr(C, "PIPELINE_WINDOWS", pipeline > 0)
+    monkeypatch.setattr(C, "PIPELINE_DEPTH", max(pipeline, 1))
     _patch_decide(monkeypatch)
     doc, res = _run(name, small_windows=small, speculate=speculate)
     assert _summary(res) == _expected(doc)
