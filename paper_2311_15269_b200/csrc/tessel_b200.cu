@@ -1002,6 +1002,7 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
   // then run subtree-parallel (sp_solve) with their real cap
   const bool sp = allow_sp && warp_mode && sp_enabled();
   std::vector<long long> real_budget(budgets);
+  if (sp) SP_FIRST = sp_env("TSL_SP_FIRST", SP_FIRST_DEFAULT);
   if (sp)
     for (int i = 0; i < count; ++i)
       if (budgets[i] == 0 || budgets[i] >= SP_MIN_BUDGET) budgets[i] = SP_FIRST;
