@@ -998,14 +998,16 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
     budgets[i] = p.node_budget < 0 ? 0 : p.node_budget;
     max_n = std::max(max_n, p.n);
   }
-  // long problems: a first pass of SP_FIRST nodes here; the ones still open
+  // long problems: a first pass of TSL_SP_BATCH_FIRST nodes here; the ones still open
   // then run subtree-parallel (sp_solve) with their real cap
   const bool sp = allow_sp && warp_mode && sp_enabled();
   std::vector<long long> real_budget(budgets);
-  if (sp) SP_FIRST = sp_env("TSL_SP_FIRST", SP_FIRST_DEFAULT);
+  // (short: the problems it leaves open restart with the subtree-parallel
+  // decide's own sample, profiles/r01i_sp_first_sweep.log)
+  const long long first = sp ? sp_env("TSL_SP_BATCH_FIRST", 1024) : 0;
   if (sp)
     for (int i = 0; i < count; ++i)
-      if (budgets[i] == 0 || budgets[i] >= SP_MIN_BUDGET) budgets[i] = SP_FIRST;
+      if (budgets[i] == 0 || budgets[i] >= SP_MIN_BUDGET) budgets[i] = first;
   if (stride < max_n) throw tsl::Error(TSL_EINVAL, "starts stride smaller than a problem size");
   DecideCtx &ctx = decide_ctx();
   std::lock_guard<std::mutex> lock(ctx.mu);
