@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import bisect
 import os
+
+import numpy as np
 from collections import deque
 import time
 from collections.abc import Sequence
@@ -21,7 +23,7 @@ from typing import Optional
 
 from .engine import (VERIFY_SLOTS, WINDOW_FIRST, WINDOW_GROWTH, WINDOW_MAX,
                      BatchedRepetendSearch)
-from .parallel import LevelSync, split_range
+from .parallel import SoloComm, split_range
 from .placement import BlockInstance, PlacementSpec
 from .repetend import (Repetend, RepetendOutcome, entry_memory, lower_bound, make_repetend,
                        steady_memory_ok)
@@ -63,24 +65,35 @@ class CandidateLog(Sequence):
         self._segs: list = []     # (n_r, r0, count)
         self._special: dict = {}  # global index -> CandidateRecord
         self._appended: list = []
+        self._pending: list = []  # (count, specials) of segments awaiting set_infeasible
         self._size = 0
         self.counts: dict = {}
 
-    def add_segment(self, n_r: int, r0: int, count: int, special: dict, infeasible: int):
-        if count <= 0:
-            return
-        base = self._size
-        self._starts.append(base)
-        self._segs.append((n_r, r0, count))
-        for off, rec in special.items():
-            self._special[base + off] = rec
-            self.counts[rec.status] = self.counts.get(rec.status, 0) + 1
-        if infeasible:
-            self.counts["infeasible"] = self.counts.get("infeasible", 0) + infeasible
-        bound = count - len(special) - infeasible
-        if bound:
-            self.counts["bound"] = self.counts.get("bound", 0) + bound
-        self._size += count
+    def add_segment(self, n_r: int, r0: int, count: int, special: dict,
+                    infeasible: Optional[int]):
+        """Window [r0, r0 + count) of n_r with its explicit records;
+        ``infeasible`` = its gate-rejected count, or None when it is supplied
+        later by ``set_infeasible`` (sharded windows: reduced at the end)."""
+        self._pending.append((count, len(special)))
+        if count > 0:
+            self._starts.append(self._size)
+            self._segs.append((n_r, r0, count))
+            for off, rec in special.items():
+                self._special[self._size + off] = rec
+                self.counts[rec.status] = self.counts.get(rec.status, 0) + 1
+            self._size += count
+        if infeasible is not None:
+            self.set_infeasible([infeasible])
+
+    def set_infeasible(self, counts):
+        """Gate-rejected counts of the segments added without one, in order."""
+        for infeasible in counts:
+            count, n_special = self._pending.pop(0)
+            if infeasible:
+                self.counts["infeasible"] = self.counts.get("infeasible", 0) + infeasible
+            bound = count - n_special - infeasible
+            if bound:
+                self.counts["bound"] = self.counts.get("bound", 0) + bound
 
     def append(self, rec: CandidateRecord):
         self._appended.append(rec)
@@ -275,7 +288,10 @@ class _Feasibility:
         self.memo: dict = {}
 
     def evaluate(self, rep: Repetend):
-        key = rep.assignment
+        # lazy checks depend on the assignment only (warmup / cooldown sets and
+        # entry memory); an eager completion also places copy 0 from the
+        # witness, so it is keyed by the whole repetend
+        key = rep.assignment if self.lazy else (rep.assignment, rep.internal, rep.period)
         if key not in self.memo:
             scratch = SearchReport(0, 0, 0, self.lazy)
             ok, sched, exc = False, None, None
@@ -313,6 +329,8 @@ PIPELINE_WINDOWS = os.environ.get("TESSEL_PIPELINE_WINDOWS", "1") == "1"
 # verification slot each, plus the slot of the window being scanned)
 PIPELINE_DEPTH = max(1, min(int(os.environ.get("TESSEL_PIPELINE_DEPTH", "3")), VERIFY_SLOTS - 1))
 
+_IMPROVED, _COMPLETION_INFEASIBLE = 1, 2
+
 
 def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optional[int] = None,
            lazy: bool = True, budget: Optional[float] = None, jobs: int = 1,
@@ -321,7 +339,18 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
     """Two-phase schedule search: repetend construction, then completion
     (completion.py:284-396).  ``jobs`` is accepted for API compatibility;
     candidate parallelism comes from the GPU windows instead of a process
-    pool.  ``device`` selects the CUDA device (default: current)."""
+    pool.  ``device`` selects the CUDA device (default: current).  ``comm``
+    (parallel.Comm) shards every window across the processes of a
+    torch.distributed group, one GPU each; every rank returns the same
+    result.
+
+    ``report.stats.decides`` is the reference's decide count (every period
+    probe its sequential scan would run, plus the completion decides);
+    ``report.stats.nodes`` counts the completion decides' nodes exactly and
+    the repetend probes' nodes as explored here (the root filter and the
+    disjunctive refutation settle most probes without the reference's DFS,
+    so its node total is not reproduced).  ``report.engine`` holds this
+    search's GPU counters."""
     cap = mem_capacity
     lb = lower_bound(p)
     total = sum(b.time_cost for b in p.blocks)
@@ -335,173 +364,262 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
         raise NoFeasibleSchedule("per-device net memory of one micro-batch must be <= 0 to repeat")
     deadline = time.monotonic() + (budget if budget is not None else default_budget())
 
+    coll = comm if comm is not None else SoloComm()
+    root = coll.rank == 0
     eng = engine if engine is not None else BatchedRepetendSearch(p, device or 0)
+    c_start = dict(eng.counters.__dict__)
     log = CandidateLog(p, cap, eng.unrank)
     report.candidates = log
     feas = _Feasibility(p, cap, lazy, deadline)
+    k = p.num_stages
 
     def feasible(n_r, rank, period, starts):
         rep = make_repetend(p, eng.unrank(n_r, rank), [int(v) for v in starts], period)
         return feas.ok(rep)
 
+    def span(opt: int) -> int:
+        """Periods the reference's scan probes for a candidate with no SAT
+        below ``opt`` (repetend.py:272-302)."""
+        return max(0, min(total, opt - 1) - lb + 1)
+
     best: Optional[Repetend] = None
     best_completed: Optional[Schedule] = None
     optimal = total + 1
     done = False
+    past_deadline = False       # agreed by every rank at each gather
+    acct = {"decides": 0, "infeasible": []}  # this rank's share, reduced at the end
     t_rep = time.monotonic()
 
     def windows():
-        """(n_r, r0, r1) in the reference's candidate order, windows growing."""
+        """(n_r, r0, r1) in the reference's candidate order, windows growing
+        (one window per rank at a time)."""
         for n_r in range(1, max(limit, 1) + 1):
             count = eng.count(n_r)
-            r0, width = 0, WINDOW_FIRST
+            r0, width = 0, WINDOW_FIRST * coll.size
             while r0 < count:
                 r1 = min(count, r0 + width)
                 yield n_r, r0, r1
                 r0 = r1
-                width = min(width * WINDOW_GROWTH, WINDOW_MAX)
+                width = min(width * WINDOW_GROWTH, WINDOW_MAX * coll.size)
+
+    def gather(r0, a0, win, optimal_now, launched=False):
+        """All shards' first SATs of a window (window-relative index ->
+        (period, starts)), the window prefix whose outcomes are known and
+        whether any shard launched a verification."""
+        nonlocal past_deadline
+        rows = np.zeros((len(win.first_sat), k + 2), dtype=np.int64)
+        for i, (w, (period, starts)) in enumerate(sorted(win.first_sat.items())):
+            rows[i, 0], rows[i, 1] = a0 - r0 + w, period
+            rows[i, 2:] = starts
+        cut = a0 - r0 + win.determined_prefix(optimal_now)
+        if not win.timed_out:
+            cut = 1 << 62
+        allrows, heads = coll.gather_rows(rows, [cut, int(time.monotonic() > deadline),
+                                                 int(launched)])
+        past_deadline = any(h[1] for h in heads)
+        cut = min(h[0] for h in heads)
+        first_sat = {int(r[0]): (int(r[1]), r[2:]) for r in allrows}
+        return first_sat, cut, any(h[2] for h in heads)
 
     def replay(n_r, r0, r1, a0, win) -> bool:
         """Ordered replay of a window's first SATs (completion.py:351-382);
-        True = the search ends (load bound reached)."""
+        True = the search ends (load bound reached or out of time)."""
         nonlocal best, best_completed, optimal
-        first_sat = {a0 - r0 + w: v for w, v in win.first_sat.items()}
-        if comm is not None:
-            merged: dict = {}
-            for part in comm.allgather(first_sat):
-                merged.update(part)
-            first_sat = merged
+        opt0 = optimal
+        first_sat, cut, _ = gather(r0, a0, win, optimal)
+        timed_out = cut < (1 << 62)
+        used = min(r1 - r0, cut)
+        msg, error = None, None
+        if root:  # the improvement rule and the completion checks, rank 0 only
+            decisions, stop, opt = [], False, optimal
+            try:
+                for widx in sorted(first_sat):
+                    if widx >= used:
+                        break
+                    period, starts = first_sat[widx]
+                    if period >= opt:
+                        continue  # first SAT beyond this candidate's bound: "bound"
+                    rep = make_repetend(p, eng.unrank(n_r, r0 + widx),
+                                        [int(v) for v in starts], period)
+                    ok, sched = feas.replay(rep, report)
+                    if ok:
+                        opt = rep.period
+                        if not lazy:
+                            best_completed = sched
+                    decisions += [widx, _IMPROVED if ok else _COMPLETION_INFEASIBLE]
+                    if ok and opt == lb:
+                        stop, used = True, widx + 1
+                        break
+            except CompletionTimeout as e:  # eager mode: fatal, as in the reference
+                error = e
+            msg = [used, int(stop), int(error is not None)] + decisions
+        msg = coll.bcast_ints(msg)
+        used, stop, decisions = msg[0], bool(msg[1]), msg[3:]
+        if msg[2]:
+            text = coll.bcast_obj(str(error) if root else None)
+            raise error if error is not None else CompletionTimeout(text)
         special: dict = {}
-        used = r1 - r0
-        stop = False
-        for widx in sorted(first_sat):
+        points = []  # (widx, bound from widx + 1 on) for the decide accounting
+        for i in range(0, len(decisions), 2):
+            widx, code = decisions[i], decisions[i + 1]
             period, starts = first_sat[widx]
-            if period >= optimal:
-                continue  # first SAT beyond this candidate's bound: "bound"
             a = eng.unrank(n_r, r0 + widx)
             rep = make_repetend(p, a, [int(v) for v in starts], period)
-            ok, sched = feas.replay(rep, report)
-            status = "completion-infeasible"
-            if ok:
+            if root:  # the reference's probes for this candidate: lb..first SAT
+                acct["decides"] += (period - lb + 1) - span(optimal)
+            if code == _IMPROVED:
                 best, optimal = rep, rep.period
-                if not lazy:
-                    best_completed = sched
                 report.improvements.append((a, optimal))
-                status = "improved"
-            special[widx] = CandidateRecord(n_r, a, rep.period, status)
-            if ok and optimal == lb:
-                stop = True
-                used = widx + 1
-                break
-        infeasible = 0
-        if win.gate is not None:
-            mine = max(0, min(win.count, r0 + used - a0))
-            infeasible = int(mine - win.gate[:mine].sum())
-            if comm is not None:
-                infeasible = comm.allreduce_sum([infeasible])[0]
-        log.add_segment(n_r, r0, used, special, infeasible)
+                points.append((widx, optimal))
+            special[widx] = CandidateRecord(n_r, a, rep.period,
+                                            "improved" if code == _IMPROVED
+                                            else "completion-infeasible")
+        # this rank's share: reference decides of every candidate that
+        # passes the memory gate, at the bound in force at its index
+        lo_w, hi_w = a0 - r0, min(a0 - r0 + win.count, used)
+        passing = (np.ones(max(0, hi_w - lo_w), dtype=np.int64) if win.gate is None
+                   else win.gate[:max(0, hi_w - lo_w)].astype(np.int64))
+        cum = np.concatenate(([0], np.cumsum(passing)))
+
+        def n_pass(i0, i1):  # window-relative [i0, i1) within this shard
+            i0, i1 = max(i0, lo_w), min(i1, hi_w)
+            return int(cum[i1 - lo_w] - cum[i0 - lo_w]) if i1 > i0 else 0
+
+        opt, prev = opt0, 0
+        for widx, new_opt in points:
+            acct["decides"] += n_pass(prev, widx + 1) * span(opt)
+            opt, prev = new_opt, widx + 1
+        acct["decides"] += n_pass(prev, used) * span(opt)
+        acct["infeasible"].append(int(len(passing) - cum[-1]))
+        log.add_segment(n_r, r0, used, special, None)
+        if timed_out and not stop:
+            report.timed_out = True
+            return True
         return stop
 
-    def predicted_optimal(n_r, r0, win, opt) -> int:
-        """The bound after replaying `win` from bound `opt` if its
+    def predicted_optimal(n_r, r0, a0, job, opt):
+        """The bound after replaying `job`'s window from bound `opt` if its
         speculation holds: the replay rule run without side effects
-        (memoised completion checks)."""
-        for widx in sorted(win.first_sat):
-            period, starts = win.first_sat[widx]
-            if period >= opt:
-                continue
-            rep = make_repetend(p, eng.unrank(n_r, r0 + widx), [int(v) for v in starts], period)
-            if feas.ok(rep):
-                opt = rep.period
-        return opt
+        (memoised completion checks); computed on rank 0 and broadcast.
+        Also whether any shard has pending probes under verification."""
+        first_sat, _, launched = gather(r0, a0, job.res, opt, job.launched)
+        if root:
+            for widx in sorted(first_sat):
+                period, starts = first_sat[widx]
+                if period >= opt:
+                    continue
+                rep = make_repetend(p, eng.unrank(n_r, r0 + widx), [int(v) for v in starts],
+                                    period)
+                if feas.ok(rep):
+                    opt = rep.period
+        return coll.bcast_ints([opt] if root else None)[0], launched
 
-    pipelined = comm is None and PIPELINE_WINDOWS and hasattr(eng, "begin_window")
+    pipelined = PIPELINE_WINDOWS and hasattr(eng, "begin_window")
     # windows scanned whose pending probes are being verified, oldest first:
-    # [n_r, r0, r1, job, bound the window was scanned under]
+    # [n_r, r0, r1, a0, job, bound the window was scanned under, predicted bound
+    #  after it, any shard verifying]
     inflight: deque = deque()
 
     def settle_head() -> bool:
         """Finish and replay the oldest window in flight; True = the search
         ends (load bound reached or out of time)."""
-        pn, p0, p1, pjob, _ = inflight.popleft()
+        pn, p0, p1, pa, pjob, _, _, _ = inflight.popleft()
         pwin = eng.finish_window(pjob, feasible)
-        if pwin.timed_out:
-            report.timed_out = True
-            return True
-        return replay(pn, p0, p1, p0, pwin)
+        return replay(pn, p0, p1, pa, pwin)
 
     def redo_mispredicted() -> bool:
         """The next window in flight was scanned under a predicted bound; a
         true bound above it (a repaired / rescanned misprediction) means it
         missed periods: redo it and every later one, in order, exactly."""
-        if not inflight or optimal <= inflight[0][4]:
+        if not inflight or optimal <= inflight[0][5]:
             return False
         redo = list(inflight)
         inflight.clear()  # their verification results are dropped
-        for rn, q0, q1, _, _ in redo:
-            win = eng.evaluate_window(rn, q0, q1, cap, optimal, feasible, deadline)
-            if win.timed_out:
-                report.timed_out = True
-                return True
-            if replay(rn, q0, q1, q0, win):
+        for rn, q0, q1, qa, qjob, _, _, _ in redo:
+            qb = qa + qjob.res.count
+            win = eng.evaluate_window(rn, qa, qb, cap, optimal, feasible, deadline)
+            if replay(rn, q0, q1, qa, win):
                 return True
         return False
 
     for n_r, r0, r1 in windows():
-        if time.monotonic() > deadline:
+        if past_deadline or (comm is None and time.monotonic() > deadline):
             report.timed_out = True
-            done = True
-            break
-        if comm is not None:  # rank-prefix shard of the window (parallel.py)
-            a0, b0 = split_range(r0, r1, comm.rank, comm.size)
-            win = eng.evaluate_window(n_r, a0, b0, cap, optimal, feasible, 0.0,
-                                      LevelSync(comm, a0 - r0))
-        elif not pipelined:
-            a0 = r0
-            win = eng.evaluate_window(n_r, r0, r1, cap, optimal, feasible, deadline)
-        else:
-            # Scan this window while the pending probes of up to
-            # PIPELINE_DEPTH earlier windows are verified (one stream each),
-            # under the bound their replays yield if their speculation holds
-            # (else the true bound is lower: the scan only did extra work);
-            # windows are settled and replayed strictly in order.
-            bound = optimal
-            for pn, p0, _, pjob, _ in inflight:
-                bound = predicted_optimal(pn, p0, pjob.res, bound)
-            busy = {e[3].slot for e in inflight}
-            slot = next(k for k in range(VERIFY_SLOTS) if k not in busy)
-            job = eng.begin_window(n_r, r0, r1, cap, bound, feasible, deadline, slot)
-            inflight.append([n_r, r0, r1, job, bound])
-            # settle the oldest while too many are in flight, and every head
-            # with nothing to verify (it settles without waiting)
-            while inflight and (len(inflight) > PIPELINE_DEPTH or not inflight[0][3].launched):
-                if settle_head() or redo_mispredicted():
-                    done = True
-                    break
-            if done:
+            break  # windows already scanned are still settled below
+        a0, b0 = split_range(r0, r1, coll.rank, coll.size)
+        if not pipelined:
+            win = eng.evaluate_window(n_r, a0, b0, cap, optimal, feasible, deadline)
+            if replay(n_r, r0, r1, a0, win):
+                done = True
                 break
             continue
-        if win.timed_out:
-            report.timed_out = True
-            done = True
-            break
-        if replay(n_r, r0, r1, a0, win):
-            done = True
+        # Scan this window while the pending probes of up to PIPELINE_DEPTH
+        # earlier windows are verified (one stream each), under the bound
+        # their replays yield if their speculation holds (else the true bound
+        # is lower: the scan only did extra work); windows are settled and
+        # replayed strictly in order.
+        bound = inflight[-1][6] if inflight else optimal
+        busy = {e[4].slot for e in inflight}
+        slot = next(s for s in range(VERIFY_SLOTS) if s not in busy)
+        job = eng.begin_window(n_r, a0, b0, cap, bound, feasible, deadline, slot)
+        after, launched = predicted_optimal(n_r, r0, a0, job, bound)
+        inflight.append([n_r, r0, r1, a0, job, bound, after, launched])
+        # settle the oldest while too many are in flight, and every head
+        # with nothing to verify (it settles without waiting)
+        while inflight and (len(inflight) > PIPELINE_DEPTH or not inflight[0][7]):
+            if settle_head() or redo_mispredicted():
+                done = True
+                break
+        if done:
             break
     while inflight and not done:
         if settle_head() or redo_mispredicted():
             break
     report.phase_secs["repetend"] += time.monotonic() - t_rep
-    c = eng.counters
-    report.engine = dict(c.__dict__)
-    report.stats.decides += c.probes
-    report.stats.nodes += c.nodes
 
+    # reduce this rank's accounting: status counts per segment and decides
+    red = coll.allreduce_sum([acct["decides"]] + acct["infeasible"])
+    log.set_infeasible(red[1:])
+    report.stats.decides += red[0]
+    c = eng.counters
+    report.engine = {key: (v - c_start[key] if isinstance(v, (int, float)) else v)
+                     for key, v in c.__dict__.items() if key != "trace"}
+    report.stats.nodes += c.nodes - c_start["nodes"]
     report.best_t_r = best.period if best else None
-    if best is None:
-        if report.timed_out:
-            return SearchResult(None, report)
-        raise NoFeasibleSchedule("no repetend candidate is schedulable under memory")
-    if lazy or best_completed is None:
-        best_completed = complete_schedule(p, best, cap, deadline, report)
-    return SearchResult(best_completed, report)
+
+    def finish():
+        nonlocal best_completed
+        if best is None:
+            if report.timed_out:
+                return None
+            raise NoFeasibleSchedule("no repetend candidate is schedulable under memory")
+        if lazy or best_completed is None:
+            best_completed = complete_schedule(p, best, cap, deadline, report)
+        return best_completed
+
+    if comm is None:
+        return SearchResult(finish(), report)
+    # rank 0 completes the schedule; every rank returns the same result
+    out = None
+    if root:
+        try:
+            s = finish()
+            out = {"entries": None if s is None else [(b.stage, b.mb, t)
+                                                      for b, t in s.entries.items()],
+                   "info": None if s is None else s.repetend}
+        except (NoFeasibleSchedule, CompletionTimeout) as e:
+            out = {"error": (type(e).__name__, str(e))}
+        out.update(diagnostics=report.diagnostics, phase_secs=report.phase_secs,
+                   stats=(report.stats.decides, report.stats.nodes, report.stats.wall_secs),
+                   timed_out=report.timed_out)
+    out = coll.bcast_obj(out)
+    report.diagnostics, report.phase_secs = out["diagnostics"], out["phase_secs"]
+    report.stats.decides, report.stats.nodes, report.stats.wall_secs = out["stats"]
+    report.timed_out = out["timed_out"]
+    if "error" in out:
+        name, msg = out["error"]
+        raise (NoFeasibleSchedule if name == "NoFeasibleSchedule" else CompletionTimeout)(msg)
+    if out["entries"] is None:
+        return SearchResult(None, report)
+    entries = {BlockInstance(st, mb): t for st, mb, t in out["entries"]}
+    return SearchResult(Schedule(p, best.n_r, entries, out["info"]), report)

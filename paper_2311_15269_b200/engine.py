@@ -132,6 +132,36 @@ class WindowResult:
     timed_out: bool = False
     first_feasible: Optional[int] = None            # lowest completion-feasible SAT widx
     retirers: set = field(default_factory=set)      # widx that lowered a retirement limit
+    # set when the scan ran out of time: levels lb..level-1 are complete for
+    # every candidate <= limit except the unverified (widx, period) pending
+    level: int = 0
+    limit: int = -1
+    pending: list = field(default_factory=list)
+
+    def determined_prefix(self, optimal: int) -> int:
+        """Window indices [0, n) whose reference outcome is already known
+        for a search whose bound before this window is ``optimal``: every
+        candidate of the prefix is gated out, retired, has its first SAT
+        with no unverified period below it, or was scanned through
+        optimal - 1 (conservative: the bound only falls during the replay)."""
+        if not self.timed_out:
+            return self.count
+        pend: dict = {}
+        for w, q in self.pending:
+            pend[w] = min(q, pend.get(w, q))
+        for w in range(self.count):
+            if self.gate is not None and not self.gate[w]:
+                continue
+            if w > self.limit:
+                return self.count  # retired by a lower completion-feasible SAT
+            fs = self.first_sat.get(w)
+            q = pend.get(w)
+            if fs is not None:
+                if q is not None and q < fs[0]:
+                    return w
+            elif (q is not None and q < optimal) or self.level < optimal:
+                return w
+        return self.count
 
 
 class BatchedRepetendSearch:
@@ -201,7 +231,7 @@ class BatchedRepetendSearch:
         stale (higher) bound than the exact sequential one: its outcomes are
         facts about (candidate, period) pairs and the ordered replay applies
         the true bound, so only work is added, never a different answer."""
-        res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, None, {})
+        res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, {})
         job = WindowJob((n_r, r0, r1, cap, bound, deadline), res, pending, slot, False)
         if pending and not res.timed_out:
             self.eng.verify_stash(slot, [x for x, _ in pending])
@@ -241,7 +271,7 @@ class BatchedRepetendSearch:
             self.counters.repaired += len(fix)
             return res
         self.counters.redo += 1  # rescan (the window is staged again) with the hints
-        return self.evaluate_window(n_r, r0, r1, cap, bound, feasible, deadline, None, hints)
+        return self.evaluate_window(n_r, r0, r1, cap, bound, feasible, deadline, hints)
 
     @staticmethod
     def _first_sats(sats) -> dict:
@@ -253,12 +283,10 @@ class BatchedRepetendSearch:
 
     def evaluate_window(self, n_r: int, r0: int, r1: int, cap: Optional[int], bound: int,
                         feasible: Callable[[int, int, int, np.ndarray], bool],
-                        deadline: float = 0.0, sync=None, hints=None) -> WindowResult:
+                        deadline: float = 0.0, hints=None) -> WindowResult:
         """Level-synchronous period scan of ranks [r0, r1) at n_r under the
         sequential bound ``bound`` in force at the window start.
         ``feasible(n_r, rank, period, starts)`` is the completion check.
-        ``sync`` (parallel.LevelSync) exchanges the retirement bound with the
-        other shards of the window; None = single shard.
 
         Speculation: deferred probes that survive the disjunctive filter
         would need the reference-exact DFS up to the reference's 400k-node cap,
@@ -276,8 +304,7 @@ class BatchedRepetendSearch:
         scanned again with every verified outcome as a hint."""
         hints = {} if hints is None else hints
         for _ in range(1 + 4 * 64):
-            res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, sync,
-                                             hints)
+            res, pending = self._scan_window(n_r, r0, r1, cap, bound, feasible, deadline, hints)
             if res.timed_out:
                 return res
             fix: dict = {}
@@ -286,9 +313,6 @@ class BatchedRepetendSearch:
                     fix[x] = (q, row)
             mispredicted = bool(fix)
             unsafe = bool(set(fix) & res.retirers)
-            if sync is not None:
-                mispredicted = sync.any(mispredicted)
-                unsafe = sync.any(unsafe)
             if not mispredicted:
                 return res
             if not unsafe and self.repair:
@@ -387,7 +411,7 @@ class BatchedRepetendSearch:
         row = np.array(starts if starts is not None else [0] * m.k, dtype=np.int32)
         return int(status), row, int(nodes)
 
-    def _scan_window(self, n_r, r0, r1, cap, bound, feasible, deadline, sync, hints):
+    def _scan_window(self, n_r, r0, r1, cap, bound, feasible, deadline, hints):
         res = WindowResult(n_r, r0, r1 - r0)
         pending = []
         n_act, gate = self.eng.stage(n_r, r0, r1, cap, want_gate=cap is not None)
@@ -399,8 +423,11 @@ class BatchedRepetendSearch:
         limit = res.count - 1
         top = min(self.total, bound - 1)
         active = n_act > 0
-        if sync is not None:
-            limit, active = sync(None, limit, n_act)
+
+        def out_of_time(level):
+            res.timed_out, res.level, res.limit, res.pending = True, level, limit, pending
+            return res, pending
+
         for period in range(self.lb, top + 1):
             if not active:
                 break
@@ -408,8 +435,7 @@ class BatchedRepetendSearch:
             if deadline:
                 left = deadline - time.monotonic()
                 if left <= 0:
-                    res.timed_out = True
-                    return res, pending
+                    return out_of_time(period)
                 budget_secs = left
             node_cap = 0 if period == self.lb else PROBE_NODES
             n_sat, widx, rows, n_act, n_def, st = self.eng.probe(
@@ -419,8 +445,7 @@ class BatchedRepetendSearch:
             self.counters.root_ms += root
             self.counters.probe_ms -= root
             if deadline and st["capped"] and time.monotonic() > deadline:
-                res.timed_out = True
-                return res, pending
+                return out_of_time(period)
             limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit, feasible)
             si, reruns = 0, 0
             while n_def and si < len(self.resolve_stages):
@@ -431,8 +456,7 @@ class BatchedRepetendSearch:
                 self.counters.add(st, self.eng.last_kernel_ms(), False,
                                   (n_r, r0, period, f"resolve{stage_budget}"))
                 if deadline and st["capped"] and time.monotonic() > deadline:
-                    res.timed_out = True
-                    return res, pending
+                    return out_of_time(period)
                 limit = self._scan_sats(res, n_r, r0, period, n_sat, widx, rows, limit,
                                         feasible)
                 si += 1
@@ -462,6 +486,4 @@ class BatchedRepetendSearch:
                                             feasible, extra=known_sat)
                 pending += [(w, period) for w in spec if w <= limit]
             active = n_act > 0
-            if sync is not None:
-                limit, active = sync(res.first_feasible, limit, n_act)
         return res, pending

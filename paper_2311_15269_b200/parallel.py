@@ -2,17 +2,24 @@
 
 One process per GPU (``torch.distributed``; NCCL over NVLink on the B200 box,
 gloo for CPU tests).  Every window of candidate ranks is split by rank prefix
-across the processes; during the level-synchronous scan the processes
-exchange ONE packed vector per stage with an all-reduce-min:
+across the processes and each process scans its share on its own GPU with no
+collective inside the scan (the reference's only parallelism is a process pool
+over candidates, completion.py:316-349).  Per window:
 
-    [lowest completion-feasible SAT global index, -(active candidates)]
+* one all-gather of fixed-width int64 rows — a 2-int header per rank
+  (row count, first undetermined index, deadline flag) followed by the
+  shard's first-SAT rows ``[window index, period, starts[K]]`` padded to the
+  largest shard;
+* rank 0 runs the ordered replay (the improvement rule and the completion
+  checks, completion.py:351-382) and broadcasts its decisions as one int64
+  vector (length-prefixed), so every rank applies the identical
+  improvements, records and bound without re-running completion checks.
 
-so each rank retires its candidates above the global first feasible SAT (a
-bound that flows from lower to higher indices only) and all
-ranks agree on when the window's scan ends.  After the window the SAT rows
-are all-gathered and every rank runs the same deterministic ordered replay,
-so the result (improvements, repetend, schedule, records) is identical on all
-ranks and equal to the single-GPU / reference result.
+The bound a shard is scanned under is the one in force at the window start: a
+shard above an improvement found in the same window only does extra work
+(its outcomes are facts about (candidate, period) pairs and the replay
+applies the true bound), never gives a different answer.  Status counts and
+reference decide counts are reduced once at the end of the search.
 """
 
 from __future__ import annotations
@@ -63,6 +70,75 @@ class Comm:
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    def gather_rows(self, rows, header):
+        """All-gather every rank's int64 ``rows`` (n_i x w) and 2-int
+        ``header``: returns (rows of all ranks in rank order, [header_i]).
+        Two fixed-size collectives: the headers + counts, then the rows
+        padded to the largest count."""
+        import numpy as np
+
+        torch = self.torch
+        rows = np.asarray(rows, dtype=np.int64)
+        w = rows.shape[1]
+        head = torch.tensor([rows.shape[0], *header], dtype=torch.int64, device=self.device)
+        heads = [torch.empty_like(head) for _ in range(self.size)]
+        self.dist.all_gather(heads, head, group=self.group)
+        heads = [[int(v) for v in h.tolist()] for h in heads]
+        n_max = max(h[0] for h in heads)
+        self.collectives += 1
+        if n_max == 0:
+            return np.zeros((0, w), dtype=np.int64), [h[1:] for h in heads]
+        buf = torch.zeros((n_max, w), dtype=torch.int64, device=self.device)
+        if rows.shape[0]:
+            buf[:rows.shape[0]] = torch.from_numpy(rows).to(self.device)
+        parts = [torch.empty_like(buf) for _ in range(self.size)]
+        self.dist.all_gather(parts, buf, group=self.group)
+        self.collectives += 1
+        out = np.concatenate([parts[r][:heads[r][0]].cpu().numpy() for r in range(self.size)])
+        return out, [h[1:] for h in heads]
+
+    def bcast_ints(self, vals):
+        """Broadcast rank 0's int list (length-prefixed; others pass None)."""
+        torch = self.torch
+        n = torch.tensor([len(vals) if self.rank == 0 else 0], dtype=torch.int64,
+                         device=self.device)
+        self.dist.broadcast(n, 0, group=self.group)
+        m = int(n.item())
+        t = (torch.tensor(list(vals), dtype=torch.int64, device=self.device) if self.rank == 0
+             else torch.empty(m, dtype=torch.int64, device=self.device))
+        if m:
+            self.dist.broadcast(t, 0, group=self.group)
+        self.collectives += 2
+        return [int(v) for v in t.tolist()]
+
+    def bcast_obj(self, obj):
+        """Broadcast one small picklable object from rank 0 (once per search:
+        the completed schedule and report fields)."""
+        box = [obj if self.rank == 0 else None]
+        self.dist.broadcast_object_list(box, 0, group=self.group)
+        self.collectives += 1
+        return box[0]
+
+
+class SoloComm:
+    """The single-process stand-in: every collective is the identity."""
+
+    rank, size, collectives = 0, 1, 0
+
+    def gather_rows(self, rows, header):
+        import numpy as np
+
+        return np.asarray(rows, dtype=np.int64), [list(header)]
+
+    def bcast_ints(self, vals):
+        return list(vals)
+
+    def bcast_obj(self, obj):
+        return obj
+
+    def allreduce_sum(self, vals):
+        return list(vals)
+
 
 def split_range(r0: int, r1: int, rank: int, size: int) -> tuple:
     """Contiguous rank-prefix share [a, b) of [r0, r1) for `rank`."""
@@ -70,21 +146,3 @@ def split_range(r0: int, r1: int, rank: int, size: int) -> tuple:
     a = r0 + (n * rank) // size
     b = r0 + (n * (rank + 1)) // size
     return a, b
-
-
-class LevelSync:
-    """Per-stage bound exchange for one rank's share of a window."""
-
-    def __init__(self, comm: Comm, offset: int):
-        self.comm, self.offset = comm, offset
-
-    def __call__(self, first_feasible: Optional[int], limit: int, n_active: int):
-        mine = BIG if first_feasible is None else self.offset + first_feasible
-        g_first, neg_active = self.comm.allreduce_min([mine, -n_active])
-        if g_first < BIG:
-            limit = min(limit, g_first - self.offset - 1)
-        return limit, -neg_active > 0
-
-    def any(self, flag: bool) -> bool:
-        """True on every rank if any rank raised `flag` (speculation verdicts)."""
-        return self.comm.allreduce_min([-int(bool(flag))])[0] < 0

@@ -106,14 +106,14 @@ class Recorder:
             json.dump({"seen": self.seen, "probes": recs}, f)
 
 
-def run_search(name, p, cap, max_nr, record=False):
+def run_search(name, p, cap, max_nr, record=False, lazy=True):
     rp = _ref_placement(p)
     rec = Recorder() if record else None
     if rec:
         RC.decide = rec
     try:
         t0 = time.perf_counter()
-        res = Rcomp.search(rp, cap, max_nr=max_nr)
+        res = Rcomp.search(rp, cap, max_nr=max_nr, lazy=lazy)
         wall = time.perf_counter() - t0
     finally:
         RC.decide = rec.orig if rec else RC.decide
@@ -130,6 +130,7 @@ def run_search(name, p, cap, max_nr, record=False):
         "placement": P.placement_to_dict(p),
         "mem_capacity": cap,
         "max_nr": max_nr,
+        "lazy": lazy,
         "lower_bound": rep.lower_bound,
         "limit": rep.max_nr,
         "inflights": rep.inflights,

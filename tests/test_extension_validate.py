@@ -85,3 +85,75 @@ def test_device_validation_matches_host(gpu, name):
         assert validate_schedule_device(bad) == validate_schedule(bad)
     init = [p.mem_capacity + 1] + [0] * (p.num_devices - 1)
     assert validate_schedule_device(e, init) == validate_schedule(e, init)
+
+
+# ---- pinned against the reference's own validate_schedule / metrics / plan
+# documents (tests/golden/make_more_goldens.py, schedule.py:77-296) ----------
+
+def _ref_cases():
+    import gzip
+    import json
+
+    from conftest import GOLDEN
+
+    with gzip.open(GOLDEN / "validate_ref.json.gz", "rt") as f:
+        return json.load(f)
+
+
+def _case_schedule(row):
+    from paper_2311_15269_b200.placement import BlockInstance, placement_from_dict
+    from paper_2311_15269_b200.schedule import RepetendInfo, Schedule
+
+    p = placement_from_dict(row["placement"])
+    entries = {BlockInstance(a, m): t for a, m, t in row["entries"]}
+    return Schedule(p, row["N"], entries, RepetendInfo(*row["repetend"]))
+
+
+def _viol(vs):
+    return [[v.kind, v.message, [[b.stage, b.mb] for b in v.instances]] for v in vs]
+
+
+def test_host_validation_matches_reference_fixtures():
+    from paper_2311_15269_b200.schedule import validate_schedule
+
+    rows = _ref_cases()
+    assert len(rows) >= 200 and any(r["violations"] for r in rows)
+    kinds = set()
+    for row in rows:
+        got = _viol(validate_schedule(_case_schedule(row), row["initial_memory"]))
+        assert got == row["violations"], (row["name"], row["N"], row["tag"])
+        kinds |= {v[0] for v in row["violations"]}
+    assert kinds == {"structure", "overlap", "memory", "dependency"}
+
+
+def test_metrics_and_plan_documents_match_reference_fixtures():
+    from fractions import Fraction
+
+    from paper_2311_15269_b200.schedule import (canonicalize_microbatch_order, compute_metrics,
+                                                plan_from_dict, plan_to_dict)
+
+    for row in _ref_cases():
+        if row["tag"] != "extended":
+            continue
+        s = _case_schedule(row)
+        m = compute_metrics(s)
+        exp = row["metrics"]
+        assert (m.makespan, list(m.per_device_busy), list(m.peak_memory)) == (
+            exp["makespan"], exp["per_device_busy"], exp["peak_memory"])
+        assert m.bubble_rate_total == Fraction(*exp["bubble_rate_total"])
+        assert m.bubble_rate_steady == (None if exp["bubble_rate_steady"] is None
+                                        else Fraction(*exp["bubble_rate_steady"]))
+        assert plan_to_dict(s) == row["plan"]
+        back = plan_from_dict(row["plan"])
+        assert back.entries == s.entries and back.repetend == s.repetend
+        assert sorted([b.stage, b.mb, t] for b, t in
+                      canonicalize_microbatch_order(s).entries.items()) == row["canonical"]
+
+
+@pytest.mark.gpu
+def test_device_validation_matches_reference_fixtures(gpu):
+    from paper_2311_15269_b200.validate import validate_schedule_device
+
+    for row in _ref_cases():
+        got = _viol(validate_schedule_device(_case_schedule(row), row["initial_memory"]))
+        assert got == row["violations"], (row["name"], row["N"], row["tag"])

@@ -113,6 +113,9 @@ def _check(doc, res):
     assert s.makespan() == doc["schedule"]["makespan"]
     counts = dict(res.report.candidates.counts)
     assert counts == doc["status_counts"]
+    # the reference's decide count (every period probe of its sequential
+    # scans plus the completion decides), reproduced exactly
+    assert res.report.stats.decides == doc["ref_stats"]["decides"]
     nonbound = [[c.n_r, list(c.assignment), c.t_r, c.status]
                 for c in (res.report.candidates[i] for i in range(len(res.report.candidates)))
                 if c.status != "bound"] if doc["n_candidates"] <= 30000 else None
@@ -123,7 +126,13 @@ def _check(doc, res):
 FAST = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "m4_cap8", "k4_k3", "v2_k4", "nn4_k3",
         "C1", "C2_3", "C3_9", "C5_2",
         # the full-size parity configs — seconds each on the B200
-        "C2_4", "C3_12", "C4a_3", "C4a_4", "C4b", "C5_3"]
+        "C2_4", "C3_12", "C4a_3", "C4a_4", "C4b", "C5_3",
+        # BASELINE configs[4] (K16) at N_R <= 4: reference golden from
+        # tests/golden/make_par_golden.py (the reference's own functions)
+        "C5_4",
+        # eager completion (completion.py:359-368) and the entry-memory gate
+        "eager_C1", "eager_C2_3", "eager_C3_9", "eager_m4_cap8", "eager_x4_demo_k3",
+        "eager_v4_demo_cap4", "gate_pairs_a_cap4", "gate_pairs_b_cap3", "gate_pairs_c_cap5"]
 # BASELINE configs[1] (8 micro-batches): its reference golden takes the CPU
 # reference hours; checked when tests/golden/search_C2_8.json is present
 SLOW_CASES = ["C2_8"]
@@ -136,7 +145,7 @@ def test_search_matches_reference(gpu, name):
 
     doc = load_search(name)
     p = placement_from_dict(doc["placement"])
-    _check(doc, search(p, doc["mem_capacity"], max_nr=doc["max_nr"]))
+    _check(doc, search(p, doc["mem_capacity"], max_nr=doc["max_nr"], lazy=doc.get("lazy", True)))
 
 
 @pytest.mark.parametrize("name", SLOW_CASES)

@@ -17,7 +17,10 @@ import pytest
 
 from conftest import GOLDEN, ROOT, load_search
 
-CASES = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "k4_k3", "m4_cap8", "C1", "v2_k4"]
+CASES = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "k4_k3", "m4_cap8", "C1", "v2_k4",
+         # eager completion (lazy=False) and entry-memory-gate goldens
+         "eager_C1", "eager_m4_cap8", "eager_x4_demo_k3", "eager_v4_demo_cap4",
+         "gate_pairs_b_cap3"]
 
 
 def _patch_decide(monkeypatch):
@@ -45,7 +48,8 @@ def _run(name, comm=None, small_windows=False, speculate=True, repair=True, stag
         eng.small_budget = 2
         eng.resolve_stages = ((0, stage),) if speculate else ((0, 8), (0, 0))
     try:
-        res = C.search(p, doc["mem_capacity"], max_nr=doc["max_nr"], engine=eng, comm=comm)
+        res = C.search(p, doc["mem_capacity"], max_nr=doc["max_nr"], engine=eng, comm=comm,
+                       lazy=doc.get("lazy", True))
     finally:
         C.WINDOW_FIRST, C.WINDOW_GROWTH = E.WINDOW_FIRST, E.WINDOW_GROWTH
     return doc, res
@@ -63,6 +67,7 @@ def _summary(res):
         "records": [[c.n_r, list(c.assignment), c.t_r, c.status] for c in res.report.candidates
                     if c.status != "bound"],
         "diagnostics": res.report.diagnostics,
+        "decides": res.report.stats.decides,
     }
 
 
@@ -72,6 +77,7 @@ def _expected(doc):
         "n_candidates": doc["n_candidates"], "entries": doc["schedule"]["entries"],
         "repetend": doc["schedule"]["repetend"], "counts": doc["status_counts"],
         "records": doc["records"], "diagnostics": doc["diagnostics"],
+        "decides": doc["ref_stats"]["decides"],
     }
 
 
@@ -154,7 +160,8 @@ def test_two_rank_sharded_search_matches_reference():
     per level, all-gathered SAT rows, identical replay on both ranks."""
     import torch.multiprocessing as mp
 
-    names = ["x4_demo_k3", "k4_k3", "m4_cap8", "v4_unit_cap4"]
+    names = ["x4_demo_k3", "k4_k3", "m4_cap8", "v4_unit_cap4", "eager_m4_cap8",
+             "gate_pairs_b_cap3"]
     with tempfile.TemporaryDirectory() as out:
         mp.spawn(_worker, args=(2, _free_port(), names, out), nprocs=2, join=True)
         for name in names:
