@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <stdexcept>
+#include <cstdlib>
 #include <string>
 #include <utility>
 #include <vector>
@@ -373,6 +374,58 @@ inline std::vector<int> rep_build(const Placement &pl) {
   put(R_DPPTR, dp_ptr);
   put(R_DP, dp);
   put(R_INTWIN, in_twins(out_ptr, out_dst, in_ptr, in_src, K));
+  {  // wrr_dfs.cuh tables (u64 masks as two ints, low word first)
+    const bool fits = K <= 64 && D <= 64;
+    std::vector<int> succm(2 * K, 0), predm(2 * K, 0), confm(2 * K, 0), devm(2 * K, 0),
+        devitm(2 * D, 0), multi(K, -1), winb;
+    auto setb = [](std::vector<int> &v, int row, int bit) {
+      v[2 * row + (bit >> 5)] |= (int)(1u << (bit & 31));
+    };
+    if (fits) {
+      for (auto &e : pl.deps) {
+        setb(succm, e.first, e.second);
+        setb(predm, e.second, e.first);
+      }
+      for (int i = 0; i < K; ++i) {
+        for (int j = 0; j < K; ++j)
+          if (i != j && (pl.mask[i] & pl.mask[j])) setb(confm, i, j);
+        for (int d = 0; d < D; ++d)
+          if ((pl.mask[i] >> d) & 1) {
+            setb(devm, i, d);
+            setb(devitm, d, i);
+          }
+      }
+      for (int a = 0; a < K; ++a) {
+        if (__builtin_popcountll(pl.mask[a]) < 2) continue;
+        // a's window rows: devices of a ascending, partners ascending; the
+        // first occurrence of a partner fixes its position
+        std::vector<int> pos(K, -1);
+        int next = 0;
+        for (int d = 0; d < D; ++d)
+          if ((pl.mask[a] >> d) & 1)
+            for (int y : dstages[d])
+              if (y != a && pos[y] < 0) pos[y] = next++;
+        multi[a] = (int)(winb.size() / (2 * K));
+        std::vector<int> tab(2 * K, 0);
+        for (int b = 0; b < K; ++b)
+          for (int c = 0; c < K; ++c)
+            if (pos[b] >= 0 && pos[c] >= 0 && pos[c] < pos[b]) setb(tab, b, c);
+        winb.insert(winb.end(), tab.begin(), tab.end());
+      }
+    }
+    put(R_SUCCM, succm);
+    put(R_PREDM, predm);
+    put(R_CONFM, confm);
+    put(R_DEVM, devm);
+    put(R_DEVITM, devitm);
+    put(R_MULTI, multi);
+    put(R_WINB, winb);
+    // bounds pack into 16-bit halves: 0 <= lo, hi <= 2A + max t < 2^15
+    const long long a_max = (long long)(K - 1) * (total + maxdur);
+    const char *mode = std::getenv("TSL_REP_DFS");  // "wrx": shared-memory warp DFS
+    pool[R_WRR] = fits && 2 * a_max + 2LL * maxdur < 32767 &&
+                          !(mode && std::string(mode) == "wrx") ? 1 : 0;
+  }
   pool[R_WORDS] = (int)pool.size();
   // value-range guard for the int32 device arithmetic: anchors reach
   // 2 (K-1)(P + max t) with P <= total.

@@ -110,6 +110,14 @@ enum {
   R_DPPTR, R_DP,
   // per in-entry: position of the out-entry naming the same node, or -1
   R_INTWIN,
+  // register-resident warp decide (wrr_dfs.cuh), K <= 64 items and D <= 64:
+  // per item u64 masks (lo word, hi word) of dependency successors /
+  // predecessors, conflicting items (= device-window partners) and devices;
+  // per device its items; per item the index of its window-order table (-1:
+  // single-device item, window order = ascending id) and, per multi-device
+  // item a, for every partner b the items whose first window row of a
+  // precedes b's (repetend.py:133-141 row order)
+  R_SUCCM, R_PREDM, R_CONFM, R_DEVM, R_DEVITM, R_MULTI, R_WINB, R_WRR,
   R_WORDS, R_HDR
 };
 

@@ -34,6 +34,7 @@
 #include "models.cuh"
 #include "dj_solve.cuh"
 #include "wrx_dfs.cuh"
+#include "wrr_dfs.cuh"
 #include "wdj_solve.cuh"
 #include "sp_dfs.cuh"
 #include "validate.cuh"
@@ -474,8 +475,35 @@ __global__ void __launch_bounds__(128) k_resolve(const int *__restrict__ gpool,
 // WRX state + snapshots + dependency lags + entry memory.
 __host__ __device__ inline int rep_warp_smem_words(const int *pool) {
   const int K = pool[R_K];
-  return ((wrx_state_words(K, pool[R_MAXDI]) + 3) & ~3) + (int)wrx_snap_words(K) +
-         (pool[R_NDEP] > 0 ? pool[R_NDEP] : 1) + pool[R_D] + 2;
+  const int wrx = ((wrx_state_words(K, pool[R_MAXDI]) + 3) & ~3) + (int)wrx_snap_words(K) +
+                  (pool[R_NDEP] > 0 ? pool[R_NDEP] : 1) + pool[R_D] + 2;
+  const int wrr = wrr_smem_words(K, pool[R_D]);
+  return wrx > wrr ? wrx : wrr;
+}
+
+// Reference-exact decide of one repetend probe by the warp: the
+// register-resident DFS (wrr_dfs.cuh) when the placement fits it, else the
+// shared-memory warp DFS (wrx_dfs.cuh).  The per-warp area `mine_s` holds
+// either layout; on SAT the witness is in w.s.
+__device__ __forceinline__ int rep_decide_warp(const int *sp, const unsigned char *a, int P,
+                                               int cap, int *mine_s, WWs &w, int *deplag,
+                                               int *init, long long budget,
+                                               unsigned long long t_end, long long *nd,
+                                               const int *lim, int widx) {
+  const int K = sp[R_K];
+  if (sp[R_WRR]) {
+    unsigned *snap = (unsigned *)mine_s;
+    int *vstack = mine_s + (K + 1) * 32 * (K > 32 ? 2 : 1);
+    int *winit = vstack + K + 1;
+    return K > 32 ? wrr_decide<2>(sp, a, P, cap, snap, vstack, winit, budget, t_end, nd, lim,
+                                  widx, w.s)
+                  : wrr_decide<1>(sp, a, P, cap, snap, vstack, winit, budget, t_end, nd, lim,
+                                  widx, w.s);
+  }
+  if ((threadIdx.x & 31) == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
+  __syncwarp();
+  const RepView v = rep_view(sp, P, cap, deplag, init);
+  return wrx_decide(v, w, budget, t_end, nd, lim, widx);
 }
 
 __global__ void __launch_bounds__(128, RESOLVE_MIN_BLOCKS) k_resolve_warp(const int *__restrict__ gpool,
@@ -568,11 +596,9 @@ __global__ void __launch_bounds__(128, RESOLVE_MIN_BLOCKS) k_resolve_warp(const 
       defer(widx);
       continue;
     }
-    if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
-    __syncwarp();
-    const RepView v = rep_view(sp, P, cap, deplag, init);
     long long nd = 0;
-    const int st = wrx_decide(v, w, rx_budget, t_end, &nd, dev_limit, widx);
+    const int st = rep_decide_warp(sp, a, P, cap, mine_s, w, deplag, init, rx_budget, t_end, &nd,
+                                   dev_limit, widx);
     if (st == RX_SAT) {
       int k = 0;
       if (lane == 0) {
@@ -716,11 +742,9 @@ __global__ void __launch_bounds__(128) k_verify_warp(const int *__restrict__ gpo
     // rows: the window's assignments stashed privately (the staged window
     // may already hold the next one); else the staged window
     const unsigned char *a = rows ? rows + (long long)vpos[t] * K : assign + (long long)widx * K;
-    if (lane == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
-    __syncwarp();
-    const RepView v = rep_view(sp, P, cap, deplag, init);
     long long nd = 0;
-    const int st = wrx_decide(v, w, vbudget[t], 0ull, &nd, lim, widx);
+    const int st = rep_decide_warp(sp, a, P, cap, mine_s, w, deplag, init, vbudget[t], 0ull, &nd,
+                                   lim, widx);
     if (lane == 0) {
       vstatus[t] = st;
       vnodes[t] = nd;

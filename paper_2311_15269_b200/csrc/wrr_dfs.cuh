@@ -1,0 +1,538 @@
+// wrr_dfs.cuh — register-resident warp decide for one repetend probe.
+//
+// Same contract as wrx_decide on a RepView (status, lex-min witness, node
+// count of kernel_c.pyx:23-508 for the probe repetend.py:160-190 builds),
+// with every per-item quantity in registers: lane l owns items l and l + 32
+// (S = 1 for K <= 32, S = 2 for K <= 64) and keeps their lo / hi / start,
+// duration, memory delta and micro-batch index; the placed / in-queue /
+// queued sets are warp-uniform 64-bit masks.  No shared-memory round trip
+// sits on the propagation chain:
+//
+//   * the FIFO queue is a sequence number per queued item; the pop is one
+//     ballot (seq == head); the popped item's bounds come by shuffle;
+//   * the popped item a relaxes its edge rows lane-parallel, one lane per
+//     partner b.  a's out-list (in-list) is its dependency rows (partners
+//     ascending) followed by its window rows (devices of a ascending, each
+//     device's stages ascending; repetend.py:133-141), so the reference's
+//     sequential order is recovered from two classes: a failure in the
+//     dependency class is the lowest failing partner, in the window class the
+//     first failing partner in a's window order (ascending for a
+//     single-device a, a precomputed "before" mask for a multi-device one);
+//     rows before the failure are applied and their first-improved targets
+//     enqueued in row order (ranks by popcount), exactly the items the
+//     sequential loop enqueues before it breaks — so the sticky in-queue
+//     flags of kernel_c.pyx:303-347 are reproduced.  Duplicate window rows
+//     of a pair (partners sharing several devices) carry the same lag, so
+//     only the first can change anything;
+//   * placement tightening (kernel_c.pyx:279-302) in conflict order
+//     (ascending), the first failing item cutting the pass and the drain
+//     clearing the flags of everything queued (kernel_c.pyx:341-347);
+//   * _mem_ok / _dev_ok (kernel_c.pyx:374-508) per item against every other
+//     item of the device: running memory at the end of each equal-time
+//     group, serial completion, the release-sorted suffix and the
+//     deadline-sorted prefix energetic bounds, each as a sum / max / min over
+//     the items at or after (before) an item in the stable sort order — the
+//     same numbers the insertion sorts produce;
+//   * per-depth snapshots: every lane stores its own (lo, hi) pair packed
+//     into one word (0 <= lo, hi < 2^15, host_build.hpp R_WRR) — restoring
+//     needs no synchronisation.
+#pragma once
+#include "models.cuh"
+#include "rx_dfs.cuh"
+
+#define WRR_FULL 0xffffffffu
+
+namespace wrr {
+
+__device__ __forceinline__ unsigned long long pool_u64(const int *sp, int off, int row) {
+  const int *p = sp + sp[off] + 2 * row;
+  return (unsigned long long)(unsigned)p[0] | ((unsigned long long)(unsigned)p[1] << 32);
+}
+template <int S>
+__device__ __forceinline__ unsigned long long ballot(bool b0, bool b1) {
+  unsigned long long m = __ballot_sync(WRR_FULL, b0);
+  if (S == 2) m |= (unsigned long long)__ballot_sync(WRR_FULL, b1) << 32;
+  return m;
+}
+// value of item i (uniform) held in slot i >> 5 of lane i & 31
+template <int S>
+__device__ __forceinline__ int bcast(const int (&r)[S], int i) {
+  const int v = (S == 2 && (i >> 5)) ? r[S - 1] : r[0];
+  return __shfl_sync(WRR_FULL, v, i & 31);
+}
+__device__ __forceinline__ int ffs64(unsigned long long m) { return __ffsll((long long)m) - 1; }
+__device__ __forceinline__ int popc64(unsigned long long m) { return __popcll(m); }
+__device__ __forceinline__ bool bit64(unsigned long long m, int i) { return (m >> i) & 1ull; }
+
+}  // namespace wrr
+
+// Per-warp shared scratch: snapshots (K + 1) x 32S words, vstack K + 1 words,
+// entry memory D words.
+__host__ __device__ inline int wrr_smem_words(int K, int D) {
+  const int S = K > 32 ? 2 : 1;
+  return (K + 1) * 32 * S + (K + 1) + (D > 0 ? D : 1);
+}
+
+template <int S>
+struct WrrState {
+  int lo[S], hi[S], sv[S], seq[S];
+  int t[S], m[S], nb[S];
+  unsigned long long placed, inq, queued;
+  int qh, qt;
+};
+
+// Enqueue the items of `e` (a subset of the partners) in the order given by
+// `before` (for item b: the items enqueued ahead of it among e).
+template <int S>
+__device__ __forceinline__ void wrr_enqueue(WrrState<S> &st, unsigned long long e,
+                                            const unsigned long long (&before)[S]) {
+  if (!e) return;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    if (wrr::bit64(e, b)) st.seq[k] = st.qt + wrr::popc64(e & before[k]);
+  }
+  st.qt += wrr::popc64(e);
+  st.queued |= e;
+  st.inq |= e;
+}
+
+// One relaxation phase of the popped item a over its out-list (OUT = true:
+// lo[b] >= base + lag) or in-list (hi[b] <= base - lag).  dep / win: the
+// partner classes; nd[k] / nw[k]: the candidate bound of the dependency /
+// window row of slot k.  Returns false on failure (bounds of the rows before
+// it applied, their targets enqueued).
+template <int S, bool OUT>
+__device__ __forceinline__ bool wrr_phase(WrrState<S> &st, unsigned long long dep,
+                                          unsigned long long win, const int (&nd)[S],
+                                          const int (&nw)[S], const int *winb /* or null */) {
+  const int lane = threadIdx.x & 31;
+  bool dfail[S], dimp[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    const bool isd = wrr::bit64(dep, b);
+    dimp[k] = isd && (OUT ? nd[k] > st.lo[k] : nd[k] < st.hi[k]);
+    dfail[k] = dimp[k] && (OUT ? nd[k] > st.hi[k] : nd[k] < st.lo[k]);
+  }
+  const unsigned long long DF = wrr::ballot<S>(dfail[0], dfail[S - 1]);
+  unsigned long long below[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    below[k] = (1ull << b) - 1ull;
+  }
+  if (DF) {  // the lowest failing partner cuts the dependency rows
+    const int f = wrr::ffs64(DF);
+    bool e[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const int b = 32 * k + lane;
+      const bool app = dimp[k] && b < f;
+      if (app) {
+        if (OUT) st.lo[k] = nd[k];
+        else st.hi[k] = nd[k];
+      }
+      e[k] = app && !wrr::bit64(st.inq, b);
+    }
+    wrr_enqueue<S>(st, wrr::ballot<S>(e[0], e[S - 1]), below);
+    return false;
+  }
+  bool ed[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    if (dimp[k]) {
+      if (OUT) st.lo[k] = nd[k];
+      else st.hi[k] = nd[k];
+    }
+    ed[k] = dimp[k] && !wrr::bit64(st.inq, b);
+  }
+  const unsigned long long Ed = wrr::ballot<S>(ed[0], ed[S - 1]);
+  // window rows: candidate improvement against the bounds after the
+  // dependency rows; failure = improvement beyond the opposite bound
+  bool wimp[S], wfail[S];
+  unsigned long long wb[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    const bool isw = wrr::bit64(win, b);
+    wimp[k] = isw && (OUT ? nw[k] > st.lo[k] : nw[k] < st.hi[k]);
+    wfail[k] = wimp[k] && (OUT ? nw[k] > st.hi[k] : nw[k] < st.lo[k]);
+    wb[k] = winb && isw ? ((unsigned long long)(unsigned)winb[2 * b] |
+                           ((unsigned long long)(unsigned)winb[2 * b + 1] << 32))
+                        : below[k];
+  }
+  const unsigned long long WF = wrr::ballot<S>(wfail[0], wfail[S - 1]);
+  unsigned long long cut = ~0ull;  // partners whose window row precedes the failure
+  if (WF) {
+    bool first[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) first[k] = wfail[k] && !(WF & wb[k]);
+    const int f = wrr::ffs64(wrr::ballot<S>(first[0], first[S - 1]));
+    if (winb) {
+      cut = (unsigned long long)(unsigned)winb[2 * f] |
+            ((unsigned long long)(unsigned)winb[2 * f + 1] << 32);
+    } else {
+      cut = (1ull << f) - 1ull;
+    }
+  }
+  bool ew[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    const bool app = wimp[k] && wrr::bit64(cut, b);
+    if (app) {
+      if (OUT) st.lo[k] = nw[k];
+      else st.hi[k] = nw[k];
+    }
+    ew[k] = app && !wrr::bit64(st.inq, b) && !wrr::bit64(Ed, b);
+  }
+  const unsigned long long Ew = wrr::ballot<S>(ew[0], ew[S - 1]);
+  wrr_enqueue<S>(st, Ed, below);
+  wrr_enqueue<S>(st, Ew, wb);
+  return !WF;
+}
+
+// FIFO propagation (kernel_c.pyx:303-340) from the queued items.
+template <int S>
+__device__ __forceinline__ bool wrr_propagate(const int *sp, WrrState<S> &st, int P) {
+  const int lane = threadIdx.x & 31;
+  while (st.queued) {
+    bool hit[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) hit[k] = st.seq[k] == st.qh && wrr::bit64(st.queued, 32 * k + lane);
+    const int a = wrr::ffs64(wrr::ballot<S>(hit[0], hit[S - 1]));
+    ++st.qh;
+    st.queued &= ~(1ull << a);
+    st.inq &= ~(1ull << a);
+    const int la = wrr::bcast<S>(st.lo, a), ha = wrr::bcast<S>(st.hi, a);
+    const int ta = wrr::bcast<S>(st.t, a), na = wrr::bcast<S>(st.nb, a);
+    const unsigned long long conf = wrr::pool_u64(sp, R_CONFM, a);
+    const int mi = sp[sp[R_MULTI] + a];
+    const int *winb = mi >= 0 ? sp + sp[R_WINB] + mi * 2 * sp[R_K] : nullptr;
+    int nd[S], nw[S];
+    // out rows a -> b: lag t_a - (n_a - n_b) P (dependency), t_a - P (window)
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      nd[k] = la + ta - (na - st.nb[k]) * P;
+      nw[k] = la + ta - P;
+    }
+    if (!wrr_phase<S, true>(st, wrr::pool_u64(sp, R_SUCCM, a), conf, nd, nw, winb)) return false;
+    // in rows b -> a: hi[b] <= hi[a] - lag(b -> a)
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      nd[k] = ha - (st.t[k] - (st.nb[k] - na) * P);
+      nw[k] = ha - (st.t[k] - P);
+    }
+    if (!wrr_phase<S, false>(st, wrr::pool_u64(sp, R_PREDM, a), conf, nd, nw, winb)) return false;
+  }
+  return true;
+}
+
+// _mem_ok(d) (kernel_c.pyx:374-425): events = placed items at s and unplaced
+// negative-delta items at lo; the running sum after every equal-time group.
+template <int S>
+__device__ __forceinline__ bool wrr_mem_ok(const int *sp, const WrrState<S> &st, int d, int init,
+                                           int cap) {
+  if (init > cap) return false;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long items = wrr::pool_u64(sp, R_DEVITM, d);
+  int tt[S], dm[S], run[S];
+  bool ev[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    const bool pl = wrr::bit64(st.placed, b);
+    ev[k] = wrr::bit64(items, b) && (pl || st.m[k] < 0);
+    tt[k] = pl ? st.sv[k] : st.lo[k];
+    dm[k] = ev[k] ? st.m[k] : 0;
+    run[k] = init;
+  }
+  for (unsigned long long it = items; it; it &= it - 1) {
+    const int j = wrr::ffs64(it);
+    const int tj = wrr::bcast<S>(tt, j), dj = wrr::bcast<S>(dm, j);
+#pragma unroll
+    for (int k = 0; k < S; ++k) run[k] += tj <= tt[k] ? dj : 0;
+  }
+  bool bad[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) bad[k] = ev[k] && run[k] > cap;
+  return !wrr::ballot<S>(bad[0], bad[S - 1]);
+}
+
+// _dev_ok(d) (kernel_c.pyx:428-508) over the device's items in the stable
+// orders (a, id) and (e, a-rank).
+template <int S>
+__device__ __forceinline__ bool wrr_dev_ok(const int *sp, const WrrState<S> &st, int d) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long items = wrr::pool_u64(sp, R_DEVITM, d);
+  if (!items) return true;
+  int ra[S], re[S], rd[S];
+  bool on[S];
+  int suf_d[S], suf_e[S], pre_d[S], pre_a[S];
+  int lim = -(1 << 30), sd = 0;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    on[k] = wrr::bit64(items, b);
+    const bool pl = wrr::bit64(st.placed, b);
+    ra[k] = pl ? st.sv[k] : st.lo[k];
+    re[k] = (pl ? st.sv[k] : st.hi[k]) + st.t[k];
+    rd[k] = st.t[k];
+    suf_d[k] = pre_d[k] = 0;
+    suf_e[k] = -(1 << 30);
+    pre_a[k] = 1 << 30;
+  }
+  for (unsigned long long it = items; it; it &= it - 1) {
+    const int j = wrr::ffs64(it);
+    const int aj = wrr::bcast<S>(ra, j), ej = wrr::bcast<S>(re, j), dj = wrr::bcast<S>(rd, j);
+    lim = ej > lim ? ej : lim;
+    sd += dj;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const int b = 32 * k + lane;
+      // j at or after b in the stable release order (dev_items ascending)
+      const bool ge = aj > ra[k] || (aj == ra[k] && j >= b);
+      if (ge) {
+        suf_d[k] += dj;
+        suf_e[k] = ej > suf_e[k] ? ej : suf_e[k];
+      }
+      // j at or before b in the stable deadline order of the release-sorted list
+      const bool le = ej < re[k] || (ej == re[k] && (j == b || !ge));
+      if (le) {
+        pre_d[k] += dj;
+        pre_a[k] = aj < pre_a[k] ? aj : pre_a[k];
+      }
+    }
+  }
+  bool bad[S];
+  int c = sd;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    bad[k] = on[k] && (ra[k] + suf_d[k] > suf_e[k] || pre_a[k] + pre_d[k] > re[k]);
+    if (on[k]) c = ra[k] + suf_d[k] > c ? ra[k] + suf_d[k] : c;
+  }
+  c = __reduce_max_sync(WRR_FULL, c);
+  return c <= lim && !wrr::ballot<S>(bad[0], bad[S - 1]);
+}
+
+// The probe (assignment `asg`, period P, memory cap `cap`; -1 = none).
+// Every lane calls it; returns the uniform status; *nodes_out; on SAT the
+// witness is written to s_out[0..K) (if non-null) and s_sm (if non-null).
+template <int S>
+__device__ int wrr_decide(const int *sp, const unsigned char *asg, int P, int cap,
+                          unsigned *snap, int *vstack, int *init, long long budget,
+                          unsigned long long t_end_ns, long long *nodes_out,
+                          const int *abort_lim, int abort_self, int *s_out) {
+  const int K = sp[R_K], D = sp[R_D];
+  const int lane = threadIdx.x & 31;
+  const int anchor = (K - 1) * (P + sp[R_MAXDUR]);
+  WrrState<S> st;
+  const unsigned long long all = K >= 64 ? ~0ull : ((1ull << K) - 1ull);
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int b = 32 * k + lane;
+    const bool v = b < K;
+    st.t[k] = v ? sp[sp[R_DUR] + b] : 0;
+    st.m[k] = v ? sp[sp[R_MEM] + b] : 0;
+    st.nb[k] = v ? (int)asg[b] : 0;
+    st.lo[k] = b == 0 ? anchor : 0;
+    st.hi[k] = b == 0 ? anchor : 2 * anchor;
+    st.sv[k] = 0;
+    st.seq[k] = b;  // root: every item queued in id order (kernel_c.pyx:158-165)
+  }
+  // entry memory per device (repetend.py:93-100)
+  for (int d = 0; d < D; ++d) {
+    const unsigned long long items = wrr::pool_u64(sp, R_DEVITM, d);
+    int e = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (wrr::bit64(items, 32 * k + lane)) e += st.m[k] * st.nb[k];
+    e = __reduce_add_sync(WRR_FULL, e);
+    if (lane == 0) init[d] = e;
+  }
+  __syncwarp();
+  st.placed = 0ull;
+  st.inq = st.queued = all;
+  st.qh = 0;
+  st.qt = K;
+  *nodes_out = 0;
+  if (!wrr_propagate<S>(sp, st, P)) return RX_UNSAT;
+  if (cap >= 0)
+    for (int d = 0; d < D; ++d)
+      if (!wrr_mem_ok<S>(sp, st, d, init[d], cap)) return RX_UNSAT;
+  for (int d = 0; d < D; ++d)
+    if (!wrr_dev_ok<S>(sp, st, d)) return RX_UNSAT;
+  if (K == 0) return RX_SAT;
+
+  const int *order = sp + sp[R_ORDER];
+  long long nodes = 0;
+  int status, depth = 0;
+  int v = wrr::bcast<S>(st.lo, order[0]);
+  for (;;) {
+    if (depth == K) {
+      status = RX_SAT;
+      break;
+    }
+    int x = order[depth];
+    const int dx = sp[sp[R_DUR] + x];
+    const int hix = wrr::bcast<S>(st.hi, x);
+    if (v > hix) {  // exhausted: back to the previous depth's snapshot
+      if (--depth < 0) {
+        status = RX_UNSAT;
+        break;
+      }
+      x = order[depth];
+      const unsigned *sn = snap + depth * 32 * S;
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const unsigned q = sn[32 * k + lane];
+        st.lo[k] = (int)(q & 0xffffu);
+        st.hi[k] = (int)(q >> 16);
+      }
+      st.placed &= ~(1ull << x);
+      v = vstack[depth] + 1;
+      continue;
+    }
+    const unsigned long long conf = wrr::pool_u64(sp, R_CONFM, x);
+    for (;;) {  // conflict jump: smallest value >= v overlapping no placed partner
+      int jump = -(1 << 30);
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const int b = 32 * k + lane;
+        if (wrr::bit64(conf & st.placed, b)) {
+          const int ey = st.sv[k] + st.t[k];
+          if (st.sv[k] - dx < v && v < ey) jump = ey > jump ? ey : jump;
+        }
+      }
+      jump = __reduce_max_sync(WRR_FULL, jump);
+      if (jump == -(1 << 30)) break;
+      v = jump;
+    }
+    if (v > hix) continue;
+    ++nodes;
+    if (budget && nodes > budget) {
+      status = RX_TIMEOUT;
+      break;
+    }
+    if (t_end_ns && (nodes & 4095) == 0 && rx_now_ns() > t_end_ns) {
+      status = RX_TIMEOUT;
+      break;
+    }
+    if (abort_lim && (nodes & 255) == 0) {
+      int l = 0;
+      if (lane == 0) l = *(volatile const int *)abort_lim;
+      l = __shfl_sync(WRR_FULL, l, 0);
+      if (abort_self > l) {
+        status = RX_ABORT;
+        break;
+      }
+    }
+    {
+      unsigned *sn = snap + depth * 32 * S;
+#pragma unroll
+      for (int k = 0; k < S; ++k)
+        sn[32 * k + lane] = (unsigned)st.lo[k] | ((unsigned)st.hi[k] << 16);
+    }
+    // place x at v; tighten its unplaced partners in ascending order
+    const unsigned long long xbit = 1ull << x;
+    bool chg[S], fail[S], c1[S];
+    int nlo[S], nhi[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const int b = 32 * k + lane;
+      if (b == x) {
+        st.sv[k] = v;
+        st.lo[k] = v;
+        st.hi[k] = v;
+      }
+      const bool act = wrr::bit64(conf & ~st.placed, b);
+      const int ty = st.t[k];
+      c1[k] = act && v - ty < st.lo[k] && st.lo[k] < v + dx;
+      nlo[k] = c1[k] ? v + dx : st.lo[k];
+      const bool f1 = c1[k] && nlo[k] > st.hi[k];
+      const bool c2 = act && !f1 && v - ty < st.hi[k] && st.hi[k] < v + dx;
+      nhi[k] = c2 ? v - ty : st.hi[k];
+      fail[k] = f1 || (c2 && nhi[k] < nlo[k]);
+      chg[k] = c1[k] || c2;
+      c1[k] = c1[k] && !f1;  // the lo part went through (its enqueue happened)
+    }
+    st.placed |= xbit;
+    const unsigned long long F = wrr::ballot<S>(fail[0], fail[S - 1]);
+    bool ok;
+    if (F) {
+      // items queued before the failing partner f: x, partners below f that
+      // changed, and f itself when its lo part went through; the drain
+      // clears their flags (kernel_c.pyx:341-347)
+      const int f = wrr::ffs64(F);
+      bool q[S];
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const int b = 32 * k + lane;
+        q[k] = !wrr::bit64(st.inq, b) && ((b < f && chg[k]) || (b == f && c1[k]));
+      }
+      const unsigned long long drained = wrr::ballot<S>(q[0], q[S - 1]) | xbit;
+      st.inq &= ~drained;
+      ok = false;
+    } else {
+      bool e[S];
+      unsigned long long below[S];
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const int b = 32 * k + lane;
+        st.lo[k] = nlo[k];
+        st.hi[k] = nhi[k];
+        e[k] = chg[k] && !wrr::bit64(st.inq, b);
+        below[k] = (1ull << b) - 1ull;
+      }
+      const unsigned long long E = wrr::ballot<S>(e[0], e[S - 1]);
+      // queue: x first (enqueued regardless of its flag), then E ascending
+#pragma unroll
+      for (int k = 0; k < S; ++k)
+        if (32 * k + lane == x) st.seq[k] = 0;
+      st.qh = 0;
+      st.qt = 1;
+      st.queued = xbit;
+      st.inq |= xbit;
+      wrr_enqueue<S>(st, E, below);
+      ok = wrr_propagate<S>(sp, st, P);
+      st.queued = 0ull;  // after a failure the leftovers keep their flags (sticky)
+    }
+    if (ok) {
+      const unsigned long long devs = wrr::pool_u64(sp, R_DEVM, x);
+      if (cap >= 0)
+        for (unsigned long long dm = devs; dm && ok; dm &= dm - 1) {
+          const int d = wrr::ffs64(dm);
+          ok = wrr_mem_ok<S>(sp, st, d, init[d], cap);
+        }
+      for (unsigned long long dm = devs; dm && ok; dm &= dm - 1)
+        ok = wrr_dev_ok<S>(sp, st, wrr::ffs64(dm));
+    }
+    if (ok) {
+      if (lane == 0) vstack[depth] = v;
+      ++depth;
+      __syncwarp();
+      if (depth < K) v = wrr::bcast<S>(st.lo, order[depth]);
+      continue;
+    }
+    const unsigned *sn = snap + depth * 32 * S;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const unsigned q = sn[32 * k + lane];
+      st.lo[k] = (int)(q & 0xffffu);
+      st.hi[k] = (int)(q >> 16);
+    }
+    st.placed &= ~xbit;
+    ++v;
+  }
+  *nodes_out = nodes;
+  if (status == RX_SAT && s_out) {
+#pragma unroll
+    for (int k = 0; k < S; ++k)
+      if (32 * k + lane < K) s_out[32 * k + lane] = st.sv[k];
+  }
+  __syncwarp();
+  return status;
+}

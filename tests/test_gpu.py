@@ -357,3 +357,77 @@ def test_search_variants_match_reference(gpu, monkeypatch, env):
         doc = load_search(name)
         p = placement_from_dict(doc["placement"])
         _check(doc, search(p, doc["mem_capacity"], max_nr=doc["max_nr"]))
+
+
+def _probe_inputs(p, a, period):
+    """The reference's probe for (assignment, period): repetend.py:160-190."""
+    from paper_2311_15269_b200.repetend import _model_for, entry_memory
+
+    m = _model_for(p)
+    m.set_assignment(a)
+    anchor = (m.k - 1) * (period + m.max_dur)
+    lo, hi = [0] * m.k, [2 * anchor] * m.k
+    if m.k:
+        lo[0] = hi[0] = anchor
+    return (m.k, m.dur, m.mask, m.mem, m.edges(period), m.order, lo, hi, p.num_devices,
+            list(entry_memory(p, a)))
+
+
+@pytest.mark.parametrize("kernel", ["wrr", "wrx"])
+def test_repetend_probe_kernel_matches_oracle(gpu, monkeypatch, kernel):
+    """k_verify_warp's per-warp decide — the register-resident DFS
+    (wrr_dfs.cuh, default) and the shared-memory one (wrx_dfs.cuh,
+    TSL_REP_DFS=wrx) — against the oracle's kernel_c restatement on random
+    (candidate, period) probes of every shape (single- and multi-device
+    blocks, K = 8..34, with and without a memory cap): status, node count
+    and witness, with node caps that end probes mid-search."""
+    import numpy as np
+
+    import oracle
+    from paper_2311_15269_b200 import _native
+    from paper_2311_15269_b200.placement import placement_from_dict
+    from paper_2311_15269_b200.workloads import WORKLOADS
+
+    if kernel == "wrx":
+        monkeypatch.setenv("TSL_REP_DFS", "wrx")
+    rng = random.Random(17)
+    cases = [(WORKLOADS[w].placement(), WORKLOADS[w].mem_capacity, n_r)
+             for w, n_r in (("C2@8", 4), ("C3@9", 3), ("C4a@4", 3), ("C4b", 5), ("C5@4", 3),
+                            ("C1", 3))]
+    for name in ("m4_cap8", "x4_demo_k3", "k4_k3", "nn4_k3", "gate_pairs_a_cap4"):
+        doc = load_search(name)
+        cases.append((placement_from_dict(doc["placement"]), doc["mem_capacity"], 3))
+    for row in json.loads((GOLDEN / "search_random.json").read_text())[:24]:
+        cases.append((placement_from_dict(row["placement"]), row["mem_capacity"], 3))
+    checked = timeouts = sats = 0
+    for p, cap, n_r in cases:
+        k = p.num_stages
+        eng = _native.Engine([p.block(s).time_cost for s in range(k)],
+                             [p.block(s).mem_delta for s in range(k)],
+                             [sum(1 << d for d in p.block(s).devices) for s in range(k)],
+                             sorted(p.deps), p.num_devices, 0)
+        try:
+            count = eng.count(n_r)
+            if count == 0:
+                continue
+            r1 = min(count, 4096)
+            eng.stage(n_r, 0, r1, cap)
+            lb = max(p.device_load(d) for d in range(p.num_devices))
+            total = sum(b.time_cost for b in p.blocks)
+            widx, per, bud = [], [], []
+            for _ in range(48):
+                widx.append(rng.randrange(r1))
+                per.append(rng.randint(lb, min(total, lb + 5)))
+                bud.append(rng.choice((60, 700, 5000, 40000)))
+            st, nd, rows = eng.verify(widx, per, bud, cap)
+            for i, (w, q, b) in enumerate(zip(widx, per, bud)):
+                a = eng.unrank(n_r, w)
+                exp = oracle.decide(*_probe_inputs(p, a, q), -1 if cap is None else cap, b)
+                got = (int(st[i]), [int(v) for v in rows[i]] if st[i] == 1 else None, int(nd[i]))
+                assert got == (exp[0], exp[1], exp[2]), (k, a, q, b)
+                checked += 1
+                timeouts += exp[0] == 2
+                sats += exp[0] == 1
+        finally:
+            eng.close()
+    assert checked > 1000 and timeouts > 50 and sats > 50, (checked, timeouts, sats)
