@@ -35,7 +35,7 @@ extern "C" {
 
 /* Maximum items per decide problem, devices per placement, stages per
  * placement handled by the batched repetend engine. */
-#define TSL_MAX_ITEMS 512
+#define TSL_MAX_ITEMS 2048
 #define TSL_MAX_DEVICES 64
 #define TSL_MAX_STAGES 64
 
@@ -189,6 +189,11 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
 /* Rows [first, first+count) of the last probe's SAT list (ascending window
  * index): window indices and starts[count*K].  Rows stay on the device until
  * the next tsl_engine_probe / tsl_engine_stage call. */
+/* Ordered walk of the last level's SAT list on the device: the SAT with the
+ * smallest window index above `after` (-1: the first) and its starts[K];
+ * *widx_out = -1 when there is none.  Replaces the host sort of
+ * completion.py:351-382's in-order scan (north_star kernel 3). */
+int tsl_engine_sat_next(tsl_engine *e, int64_t after, int64_t *widx_out, int32_t *starts_out);
 int tsl_engine_sat_rows(tsl_engine *e, int64_t first, int64_t count, int64_t *widx_out,
                         int32_t *starts_out);
 

@@ -82,7 +82,8 @@ EXPORTS = (
     "tsl_last_error", "tsl_version", "tsl_device_count", "tsl_set_device", "tsl_decide",
     "tsl_decide_batch", "tsl_engine_open", "tsl_engine_close", "tsl_engine_count",
     "tsl_engine_unrank", "tsl_engine_stage", "tsl_engine_probe", "tsl_engine_resolve",
-    "tsl_engine_sat_rows", "tsl_engine_take_deferred", "tsl_engine_add_active",
+    "tsl_engine_sat_rows", "tsl_engine_sat_next", "tsl_engine_take_deferred",
+    "tsl_engine_add_active",
     "tsl_engine_verify", "tsl_engine_verify_stash", "tsl_engine_verify_launch",
     "tsl_engine_verify_wait", "tsl_engine_dj", "tsl_validate",
     "tsl_engine_last_kernel_ms", "tsl_engine_last_root_ms", "tsl_counters", "tsl_sp_stats",
@@ -131,6 +132,8 @@ def lib():
     L.tsl_engine_dj.argtypes = [vp, i64, vp, vp, i64, i64, i32, vp, vp]
     L.tsl_engine_sat_rows.restype = i32
     L.tsl_engine_sat_rows.argtypes = [vp, i64, i64, vp, vp]
+    L.tsl_engine_sat_next.restype = i32
+    L.tsl_engine_sat_next.argtypes = [vp, i64, vp, vp]
     L.tsl_counters.restype = None
     L.tsl_counters.argtypes = [vp, vp, vp]
     L.tsl_engine_last_kernel_ms.restype = ctypes.c_float
@@ -402,6 +405,14 @@ class Engine:
                                         -1 if cap is None else int(cap), int(budget), int(mode),
                                         _ptr(st), _ptr(nd)))
         return st[:n].copy(), nd[:n].copy()
+
+    def sat_next(self, after: int):
+        """The level's SAT with the smallest window index above `after`
+        (device argmin) -> (widx, starts[K]) or None."""
+        w = np.zeros(1, dtype=np.int64)
+        row = np.zeros(self.K, dtype=np.int32)
+        check(self._L.tsl_engine_sat_next(self._h, int(after), _ptr(w), _ptr(row)))
+        return None if w[0] < 0 else (int(w[0]), row)
 
     def sat_rows(self, first: int, count: int):
         widx = np.zeros(max(count, 1), dtype=np.int64)

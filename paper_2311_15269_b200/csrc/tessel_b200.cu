@@ -823,6 +823,51 @@ __global__ void k_gather_rows(const int *__restrict__ rows, const int *__restric
   out[t] = rows[(long long)pos[r] * K + i];
 }
 
+// Ordered SAT walk (north_star kernel 3): the smallest window index above
+// `after` among the level's SAT rows — a lexicographic (window index, row
+// position) argmin by warp shuffles, a shared-memory pass over the warps and
+// one 64-bit atomicMin per block — then its row fetched for the host.  The
+// host replays SATs in window order up to the first completion-feasible one
+// (completion.py:351-382), so typically one argmin per level crosses PCIe.
+__global__ void __launch_bounds__(256) k_sat_min(const int *__restrict__ sat_widx, int n,
+                                                 int after, unsigned long long *key) {
+  unsigned long long best = ~0ull;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int w = sat_widx[i];
+    if (w > after) {
+      const unsigned long long k = ((unsigned long long)(unsigned)w << 32) | (unsigned)i;
+      best = k < best ? k : best;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+    best = other < best ? other : best;
+  }
+  __shared__ unsigned long long wmin[8];
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = threadIdx.x < (blockDim.x >> 5) ? wmin[threadIdx.x] : ~0ull;
+    for (int o = 4; o; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other < best ? other : best;
+    }
+    if (threadIdx.x == 0 && best != ~0ull) atomicMin(key, best);
+  }
+}
+
+__global__ void k_sat_fetch(const unsigned long long *__restrict__ key,
+                            const int *__restrict__ sat_starts, int K, int *out) {
+  const unsigned long long k = *key;
+  if (k == ~0ull) {
+    if (threadIdx.x == 0) out[0] = -1;
+    return;
+  }
+  const long long pos = (long long)(k & 0xffffffffu);
+  if (threadIdx.x == 0) out[0] = (int)(k >> 32);
+  for (int i = threadIdx.x; i < K; i += blockDim.x) out[1 + i] = sat_starts[pos * K + i];
+}
+
 // ------------------------------------------------------------------ SP-DFS
 // Speculative subtree-parallel decide for one long general problem
 // (sp_dfs.cuh): the master walk (one warp) and the subtree tasks (one warp
@@ -1024,7 +1069,9 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
   }
   // long problems: a first pass of TSL_SP_BATCH_FIRST nodes here; the ones still open
   // then run subtree-parallel (sp_solve) with their real cap
-  const bool sp = allow_sp && warp_mode && sp_enabled();
+  // (the subtree-parallel workspace holds 2 n (n + 1) ints per task warp:
+  // problems above SP_MAX_N stay one warp each)
+  const bool sp = allow_sp && warp_mode && sp_enabled() && max_n <= SP_MAX_N;
   std::vector<long long> real_budget(budgets);
   // (short: the problems it leaves open restart with the subtree-parallel
   // decide's own sample, profiles/r01i_sp_first_sweep.log)
@@ -1163,9 +1210,13 @@ struct tsl_engine {
   int *d_sat_widx = nullptr, *d_sat_starts = nullptr;
   int *d_counters = nullptr;
   unsigned long long *d_stats = nullptr;
-  // SAT rows of the last probe, sorted by window index (host) with their
-  // positions in d_sat_starts; rows are gathered on demand
+  // SAT rows of the level: the ordered walk runs on the device
+  // (k_sat_min / k_sat_fetch, tsl_engine_sat_next); the host-sorted index is
+  // built only for the legacy tsl_engine_sat_rows
   std::vector<int> sat_widx_sorted, sat_pos_sorted;
+  bool sat_sorted = false;
+  unsigned long long *d_sat_key = nullptr;
+  int *d_sat_next = nullptr;
   int *d_gather = nullptr;
   size_t d_gather_cap = 0;
   char *d_verify = nullptr;
@@ -1279,7 +1330,8 @@ struct tsl_engine {
     for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
                     (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather,
-                    (void *)d_def[0], (void *)d_def[1], (void *)d_verify, (void *)d_surv})
+                    (void *)d_def[0], (void *)d_def[1], (void *)d_verify, (void *)d_surv,
+                    (void *)d_sat_key, (void *)d_sat_next})
       if (p) cudaFree(p);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -1471,28 +1523,23 @@ static void fill_stats(const unsigned long long *st, tsl_level_stats *stats) {
   stats->dj_nodes = (int64_t)st[7];
 }
 
-// Fetch the SAT count of the level, sort the (window index, row) list on the
-// host and return the first max_sat rows.
+// Record the level's SAT count and return its first min(n_sat, max_sat)
+// rows in window order through the device argmin.
 static int finish_level(tsl_engine *e, int n_sat, int64_t max_sat, int64_t *out_nsat,
                         int64_t *sat_widx, int32_t *sat_starts) {
-  std::vector<int> widx(n_sat);
-  if (n_sat > 0) {
-    d2h(widx.data(), e->d_sat_widx, n_sat * sizeof(int), e->stream);
-    CK(cudaStreamSynchronize(e->stream));
-  }
-  std::vector<int> perm(n_sat);
-  std::iota(perm.begin(), perm.end(), 0);
-  std::sort(perm.begin(), perm.end(), [&](int x, int y) { return widx[x] < widx[y]; });
-  e->sat_widx_sorted.resize(n_sat);
-  e->sat_pos_sorted.resize(n_sat);
-  for (int r = 0; r < n_sat; ++r) {
-    e->sat_widx_sorted[r] = widx[perm[r]];
-    e->sat_pos_sorted[r] = perm[r];
-  }
   e->n_sat = n_sat;
+  e->sat_sorted = false;
   *out_nsat = n_sat;
   const long long keep = std::min<long long>(n_sat, max_sat < 0 ? 0 : max_sat);
-  if (keep > 0) return tsl_engine_sat_rows(e, 0, keep, sat_widx, sat_starts);
+  const int K = e->pool[R_K];
+  long long after = -1;
+  for (long long r = 0; r < keep; ++r) {
+    int64_t w = -1;
+    const int rc = tsl_engine_sat_next(e, after, &w, sat_starts + r * K);
+    if (rc != TSL_OK) return rc;
+    sat_widx[r] = w;
+    after = w;
+  }
   return TSL_OK;
 }
 
@@ -1920,9 +1967,57 @@ int tsl_engine_verify_wait(tsl_engine *e, int slot, int32_t *status_out, int64_t
   API_END
 }
 
+int tsl_engine_sat_next(tsl_engine *e, int64_t after, int64_t *widx_out, int32_t *starts_out) {
+  API_BEGIN
+  const int K = e->pool[R_K];
+  *widx_out = -1;
+  if (e->n_sat <= 0) return TSL_OK;
+  if (!e->d_sat_key) {
+    CK(cudaMalloc(&e->d_sat_key, sizeof(unsigned long long)));
+    CK(cudaMalloc(&e->d_sat_next, (size_t)(K + 1) * sizeof(int)));
+  }
+  CK(cudaMemsetAsync(e->d_sat_key, 0xff, sizeof(unsigned long long), e->stream));
+  const long long n = e->n_sat;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148);
+  COUNT_LAUNCH();
+  k_sat_min<<<blocks, 256, 0, e->stream>>>(e->d_sat_widx, (int)n,
+                                           (int)std::min<int64_t>(after, 0x7fffffff),
+                                           e->d_sat_key);
+  CK(cudaGetLastError());
+  COUNT_LAUNCH();
+  k_sat_fetch<<<1, 64, 0, e->stream>>>(e->d_sat_key, e->d_sat_starts, K, e->d_sat_next);
+  CK(cudaGetLastError());
+  std::vector<int> out(K + 1);
+  d2h(out.data(), e->d_sat_next, (K + 1) * sizeof(int), e->stream);
+  CK(cudaStreamSynchronize(e->stream));
+  *widx_out = out[0];
+  if (out[0] >= 0)
+    for (int i = 0; i < K; ++i) starts_out[i] = out[1 + i];
+  return TSL_OK;
+  API_END
+}
+
 int tsl_engine_sat_rows(tsl_engine *e, int64_t first, int64_t count, int64_t *widx_out,
                         int32_t *starts_out) {
   API_BEGIN
+  if (!e->sat_sorted) {  // legacy path: host-sorted index of the level's SAT list
+    const int n_sat = (int)e->n_sat;
+    std::vector<int> widx(n_sat);
+    if (n_sat > 0) {
+      d2h(widx.data(), e->d_sat_widx, n_sat * sizeof(int), e->stream);
+      CK(cudaStreamSynchronize(e->stream));
+    }
+    std::vector<int> perm(n_sat);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::sort(perm.begin(), perm.end(), [&](int x, int y) { return widx[x] < widx[y]; });
+    e->sat_widx_sorted.resize(n_sat);
+    e->sat_pos_sorted.resize(n_sat);
+    for (int r = 0; r < n_sat; ++r) {
+      e->sat_widx_sorted[r] = widx[perm[r]];
+      e->sat_pos_sorted[r] = perm[r];
+    }
+    e->sat_sorted = true;
+  }
   const long long n_sat = (long long)e->sat_widx_sorted.size();
   if (first < 0 || count < 0 || first + count > n_sat)
     throw tsl::Error(TSL_EINVAL, "SAT row range out of bounds");

@@ -39,7 +39,7 @@ WINDOW_FIRST = 2048
 WINDOW_GROWTH = 4
 WINDOW_MAX = 1 << 21
 VERIFY_SLOTS = 4      # asynchronous verification slots (TSL_VERIFY_SLOTS)
-SAT_CHUNK = 256
+SAT_CHUNK = 1        # SAT rows returned with a level (the rest: device argmin walk)
 SMALL_BUDGET = 64     # first-pass RX-DFS nodes per probe (thread per probe) before deferral
 # node cap of the concurrent verify pass; longer probes run one at a time
 # through the decide path (subtree-parallel for unlimited / >= 1M caps).
@@ -188,22 +188,27 @@ class BatchedRepetendSearch:
         self._last_ms = 0.0
 
     def _scan_sats(self, res, n_r, r0, period, n_sat, widx, rows, limit, feasible, extra=()):
-        """Walk the level's SAT rows (device list, already sorted, merged with
-        host-known SATs `extra`) in window order up to the first
-        completion-feasible one; it retires every higher index."""
-        dev = []
-        i, start = 0, 0
-        while i < n_sat:
-            if i >= start + len(widx):
-                start = i
-                widx, rows = self.eng.sat_rows(i, min(SAT_CHUNK, n_sat - i))
-            j = i - start
-            w = int(widx[j])
-            if w > limit:
+        """Walk the level's SATs in window order — the device's ordered
+        argmin (the first row comes with the level's result, each next one
+        from ``sat_next``), merged with host-known SATs `extra` — up to the
+        first completion-feasible one; it retires every higher index."""
+        ex = sorted(extra, key=lambda r: r[0])
+        xi = 0
+        dev = (int(widx[0]), rows[0]) if n_sat and len(widx) else None
+        fetch = n_sat > 0 and dev is None  # the next device SAT is still to be fetched
+        last, taken = -1, 0
+        while True:
+            if fetch:
+                dev = self.eng.sat_next(last) if taken < n_sat else None
+                fetch = False
+            if dev is None and xi >= len(ex):
                 break
-            dev.append((w, rows[j]))
-            i += 1
-        for w, row in sorted(list(extra) + dev, key=lambda r: r[0]):
+            if xi >= len(ex) or (dev is not None and dev[0] < ex[xi][0]):
+                w, row = dev
+                last, dev, fetch, taken = w, None, True, taken + 1
+            else:
+                w, row = ex[xi]
+                xi += 1
             if w > limit:
                 break
             res.first_sat[w] = (period, np.array(row, dtype=np.int32).copy())

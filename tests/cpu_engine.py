@@ -179,6 +179,10 @@ class OracleEngine:
     def verify_wait(self, slot):
         return self._vres[slot]
 
+    def sat_next(self, after):
+        later = sorted((w, s) for w, s in self.sats if w > after)
+        return (later[0][0], np.array(later[0][1], dtype=np.int32)) if later else None
+
     def sat_rows(self, first, count):
         self.sats.sort(key=lambda r: r[0])
         part = self.sats[first:first + count]
