@@ -220,6 +220,15 @@ def _roofline(kernel_ms: dict, steps: int, workload: str):
            "kernel_ms_per_step": {k: v / steps for k, v in kernel_ms.items()},
            "peak_basis": f"148 SMs x 4 issue/clk x {mhz} MHz (MEASURED_PEAKS sm_max_mhz)",
            "achieved": None, "frac": None, "traffic": None}
+    ip = ROOT / "profiles" / "r02_int_peak.json"
+    if ip.exists():  # INT32 lane throughput measured on the box (scripts/int_peak.cu)
+        d = json.loads(ip.read_text())
+        out["int32_measured"] = {
+            "lop3_lanes_per_sm_clk": d["lop3_lanes_per_sm_clk"],
+            "iadd3_lanes_per_sm_clk": d["iadd_lanes_per_sm_clk"],
+            "alu_warp_inst_peak_per_s": d["lop3_ops_per_s"] / 32,
+            "basis": "scripts/int_peak.cu on a B200 (profiles/r02_int_peak.json): the ALU "
+                     "pipe retires 64 int32 lanes/SM/clk = half the warp-issue peak"}
     prof = ROOT / "profiles" / "inst_counts.json"
     if prof.exists():
         d = json.loads(prof.read_text())

@@ -98,7 +98,11 @@ def lib():
     if not LIB_PATH.exists():
         raise NativeError(-2, f"{LIB_PATH.name} is not built; run __graft_entry__.build() "
                               "(there is no CPU fallback)")
-    L = ctypes.CDLL(str(LIB_PATH))
+    path = LIB_PATH
+    variant = os.environ.get("TSL_LIB_VARIANT")  # experiments: an alternately compiled build
+    if variant:
+        path = PKG / f"libtessel_b200_{variant}.so"
+    L = ctypes.CDLL(str(path))
     vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     L.tsl_last_error.restype = ctypes.c_char_p
     L.tsl_version.restype = i32

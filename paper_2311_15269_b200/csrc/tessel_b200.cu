@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(256, 4) k_dj_filter(const int *__restrict__ gp
 // pairs, one warp each, reference-exact DFS under the reference cap for that
 // period (0 = none at the load bound).  Writes status / nodes / starts per
 // pair (no list compaction: the host owns the bookkeeping).
-__global__ void __launch_bounds__(128) k_verify_warp(const int *__restrict__ gpool,
+__global__ void __launch_bounds__(128, 1) k_verify_warp(const int *__restrict__ gpool,
                                                      const unsigned char *__restrict__ assign,
                                                      const int *__restrict__ vwidx,
                                                      const int *__restrict__ vper,

@@ -257,14 +257,21 @@ __device__ __forceinline__ bool wrr_propagate(const int *sp, WrrState<S> &st, in
 
 // _mem_ok(d) (kernel_c.pyx:374-425): events = placed items at s and unplaced
 // negative-delta items at lo; the running sum after every equal-time group.
+// Device item tables: per device its item mask (two words) and its items
+// ascending (dev_ptr / dev_items), so the pairwise loops below have a known
+// trip count and independent iterations (unrolled: shuffles overlap).
+struct WrrDev {
+  const int *itm, *ptr, *items;
+};
+
 template <int S>
-__device__ __forceinline__ bool wrr_mem_ok(const int *sp, const WrrState<S> &st, int d, int init,
-                                           int cap) {
+__device__ __forceinline__ bool wrr_mem_ok(const WrrDev &dv, const WrrState<S> &st, int d,
+                                           int init, int cap) {
   typedef wrr::Mask<S> Mk;
   typedef typename Mk::T M;
   if (init > cap) return false;
   const int lane = threadIdx.x & 31;
-  const M items = wrr::row<S>(sp, R_DEVITM, d);
+  const M items = Mk::load(dv.itm + 2 * d);
   int tt[S], dm[S], run[S];
   bool ev[S];
 #pragma unroll
@@ -276,8 +283,10 @@ __device__ __forceinline__ bool wrr_mem_ok(const int *sp, const WrrState<S> &st,
     dm[k] = ev[k] ? st.m[k] : 0;
     run[k] = init;
   }
-  for (M it = items; it; it &= it - 1) {
-    const int j = Mk::ffs(it);
+  const int pe = dv.ptr[d + 1];
+#pragma unroll 4
+  for (int p = dv.ptr[d]; p < pe; ++p) {
+    const int j = dv.items[p];
     const int tj = wrr::bcast<S>(tt, j), dj = wrr::bcast<S>(dm, j);
 #pragma unroll
     for (int k = 0; k < S; ++k) run[k] += tj <= tt[k] ? dj : 0;
@@ -291,11 +300,11 @@ __device__ __forceinline__ bool wrr_mem_ok(const int *sp, const WrrState<S> &st,
 // _dev_ok(d) (kernel_c.pyx:428-508) over the device's items in the stable
 // orders (a, id) and (e, a-rank).
 template <int S>
-__device__ __forceinline__ bool wrr_dev_ok(const int *sp, const WrrState<S> &st, int d) {
+__device__ __forceinline__ bool wrr_dev_ok(const WrrDev &dv, const WrrState<S> &st, int d) {
   typedef wrr::Mask<S> Mk;
   typedef typename Mk::T M;
   const int lane = threadIdx.x & 31;
-  const M items = wrr::row<S>(sp, R_DEVITM, d);
+  const M items = Mk::load(dv.itm + 2 * d);
   if (!items) return true;
   int ra[S], re[S];
   unsigned pk[S];
@@ -314,8 +323,10 @@ __device__ __forceinline__ bool wrr_dev_ok(const int *sp, const WrrState<S> &st,
     suf_e[k] = -(1 << 30);
     pre_a[k] = 1 << 30;
   }
-  for (M it = items; it; it &= it - 1) {
-    const int j = Mk::ffs(it);
+  const int pe = dv.ptr[d + 1];
+#pragma unroll 4
+  for (int p = dv.ptr[d]; p < pe; ++p) {
+    const int j = dv.items[p];
     const unsigned pj = wrr::bcastu<S>(pk, j);
     const int aj = (int)(pj & 0xffffu), ej = (int)(pj >> 16), dj = wrr::bcast<S>(st.t, j);
     lim = ej > lim ? ej : lim;
@@ -397,12 +408,14 @@ __device__ int wrr_decide(const int *sp, const unsigned char *asg, int P, int ca
   st.qh = 0;
   st.qt = K;
   *nodes_out = 0;
+  const WrrDev dv{sp + sp[R_DEVITM], sp + sp[R_DEVPTR], sp + sp[R_DEVITEMS]};
+  const int *devm = sp + sp[R_DEVM], *dur = sp + sp[R_DUR];
   if (!wrr_propagate<S>(sp, st, P)) return RX_UNSAT;
   if (cap >= 0)
     for (int d = 0; d < D; ++d)
-      if (!wrr_mem_ok<S>(sp, st, d, init[d], cap)) return RX_UNSAT;
+      if (!wrr_mem_ok<S>(dv, st, d, init[d], cap)) return RX_UNSAT;
   for (int d = 0; d < D; ++d)
-    if (!wrr_dev_ok<S>(sp, st, d)) return RX_UNSAT;
+    if (!wrr_dev_ok<S>(dv, st, d)) return RX_UNSAT;
   if (K == 0) return RX_SAT;
 
   const int *order = sp + sp[R_ORDER];
@@ -433,7 +446,7 @@ __device__ int wrr_decide(const int *sp, const unsigned char *asg, int P, int ca
       v = vstack[depth] + 1;
       continue;
     }
-    const int dx = sp[sp[R_DUR] + x];
+    const int dx = dur[x];
     bool cf[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) cf[k] = wrr::bit(st.conf[k], x);
@@ -534,13 +547,13 @@ __device__ int wrr_decide(const int *sp, const unsigned char *asg, int P, int ca
       st.queued = 0;  // after a failure the leftovers keep their flags (sticky)
     }
     if (ok) {
-      const M devs = wrr::row<S>(sp, R_DEVM, x);
+      const M devs = Mk::load(devm + 2 * x);
       if (cap >= 0)
         for (M dm = devs; dm && ok; dm &= dm - 1) {
           const int d = Mk::ffs(dm);
-          ok = wrr_mem_ok<S>(sp, st, d, init[d], cap);
+          ok = wrr_mem_ok<S>(dv, st, d, init[d], cap);
         }
-      for (M dm = devs; dm && ok; dm &= dm - 1) ok = wrr_dev_ok<S>(sp, st, Mk::ffs(dm));
+      for (M dm = devs; dm && ok; dm &= dm - 1) ok = wrr_dev_ok<S>(dv, st, Mk::ffs(dm));
     }
     if (ok) {
       if (lane == 0) vstack[depth] = v;

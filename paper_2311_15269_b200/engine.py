@@ -47,7 +47,7 @@ SMALL_BUDGET = 64     # first-pass RX-DFS nodes per probe (thread per probe) bef
 # for the speculation to pay (tests/native/sp_sim.cpp model), so they stay
 # one warp each, all concurrently.
 VERIFY_FIRST = int(os.environ.get("TESSEL_VERIFY_FIRST", str(1 << 40)))
-DJ_BUDGET = 200_000   # disjunctive-refutation nodes per deferred probe
+DJ_BUDGET = int(os.environ.get("TESSEL_DJ_BUDGET", "200000"))  # disjunctive nodes per deferred probe
 # escalation of deferred probes: (DJ budget, RX-DFS stage budget; 0 = the
 # reference cap).  The retirement limit is re-applied between stages, so a
 # probe above the lowest completion-feasible SAT never runs the full cap.

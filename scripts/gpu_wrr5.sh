@@ -1,0 +1,9 @@
+set -x
+export TESSEL_BUDGET_SECS=1e9
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/wrr_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu.py -q -x -k "repetend_probe_kernel or search_matches_reference" --durations=6 2>&1 | tail -6 > gpurun_out/wrr5_tests.log
+: > gpurun_out/wrr5_traces.log
+for w in C2@4 C3@9 C5@4 C4a@3 C4a@4 C3@12 C2@8; do
+  TRACE_OUT=gpurun_out/trace_$w.json timeout 600 python scripts/trace_search.py $w > gpurun_out/tr.tmp 2>&1; head -1 gpurun_out/tr.tmp >> gpurun_out/wrr5_traces.log
+done
