@@ -425,6 +425,8 @@ inline std::vector<int> rep_build(const Placement &pl) {
     const char *mode = std::getenv("TSL_REP_DFS");  // "wrx": shared-memory warp DFS
     pool[R_WRR] = fits && 2 * a_max + 2LL * maxdur < 32767 &&
                           !(mode && std::string(mode) == "wrx") ? 1 : 0;
+    const char *strong = std::getenv("TSL_REP_STRONG");  // "0": exact DFS only
+    pool[R_WST] = pool[R_WRR] && maxdi <= 8 && !(strong && std::string(strong) == "0") ? 1 : 0;
   }
   pool[R_WORDS] = (int)pool.size();
   // value-range guard for the int32 device arithmetic: anchors reach

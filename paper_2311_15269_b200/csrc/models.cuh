@@ -118,6 +118,8 @@ enum {
   // item a, for every partner b the items whose first window row of a
   // precedes b's (repetend.py:133-141 row order)
   R_SUCCM, R_PREDM, R_CONFM, R_DEVM, R_DEVITM, R_MULTI, R_WINB, R_WRR,
+  // 1: repetend probes run the strong search first (wst_dfs.cuh)
+  R_WST,
   R_WORDS, R_HDR
 };
 

@@ -35,6 +35,7 @@
 #include "dj_solve.cuh"
 #include "wrx_dfs.cuh"
 #include "wrr_dfs.cuh"
+#include "wst_dfs.cuh"
 #include "wdj_solve.cuh"
 #include "sp_dfs.cuh"
 #include "validate.cuh"
@@ -485,20 +486,38 @@ __host__ __device__ inline int rep_warp_smem_words(const int *pool) {
 // register-resident DFS (wrr_dfs.cuh) when the placement fits it, else the
 // shared-memory warp DFS (wrx_dfs.cuh).  The per-warp area `mine_s` holds
 // either layout; on SAT the witness is in w.s.
+// `full_budget` is the reference's cap for the probe (0 = none, at the load
+// bound); `budget` the node budget of this run (a resolve stage may run
+// below the cap).  With the strong search (wst_dfs.cuh) first, only a SAT
+// found within the cap of a capped probe needs the exact count.
 __device__ __forceinline__ int rep_decide_warp(const int *sp, const unsigned char *a, int P,
                                                int cap, int *mine_s, WWs &w, int *deplag,
                                                int *init, long long budget,
                                                unsigned long long t_end, long long *nd,
-                                               const int *lim, int widx) {
+                                               const int *lim, int widx,
+                                               long long full_budget) {
   const int K = sp[R_K];
   if (sp[R_WRR]) {
     unsigned *snap = (unsigned *)mine_s;
     int *vstack = mine_s + (K + 1) * 32 * (K > 32 ? 2 : 1);
     int *winit = vstack + K + 1;
-    return K > 32 ? wrr_decide<2>(sp, a, P, cap, snap, vstack, winit, budget, t_end, nd, lim,
-                                  widx, w.s)
-                  : wrr_decide<1>(sp, a, P, cap, snap, vstack, winit, budget, t_end, nd, lim,
-                                  widx, w.s);
+    long long n1 = 0;
+    if (sp[R_WST]) {
+      const int st = K > 32 ? wst_decide<2>(sp, a, P, cap, snap, vstack, winit, budget, t_end,
+                                            &n1, lim, widx, w.s)
+                            : wst_decide<1>(sp, a, P, cap, snap, vstack, winit, budget, t_end,
+                                            &n1, lim, widx, w.s);
+      if (st != RX_SAT || full_budget == 0) {
+        *nd = n1;
+        return st;
+      }
+    }
+    const int st = K > 32 ? wrr_decide<2>(sp, a, P, cap, snap, vstack, winit, budget, t_end,
+                                          nd, lim, widx, w.s)
+                          : wrr_decide<1>(sp, a, P, cap, snap, vstack, winit, budget, t_end,
+                                          nd, lim, widx, w.s);
+    *nd += n1;
+    return st;
   }
   if ((threadIdx.x & 31) == 0) rep_prepare(sp, a, P, deplag, init, w.lo, w.hi);
   __syncwarp();
@@ -598,7 +617,7 @@ __global__ void __launch_bounds__(128, RESOLVE_MIN_BLOCKS) k_resolve_warp(const 
     }
     long long nd = 0;
     const int st = rep_decide_warp(sp, a, P, cap, mine_s, w, deplag, init, rx_budget, t_end, &nd,
-                                   dev_limit, widx);
+                                   dev_limit, widx, full_budget);
     if (st == RX_SAT) {
       int k = 0;
       if (lane == 0) {
@@ -744,7 +763,7 @@ __global__ void __launch_bounds__(128, 1) k_verify_warp(const int *__restrict__ 
     const unsigned char *a = rows ? rows + (long long)vpos[t] * K : assign + (long long)widx * K;
     long long nd = 0;
     const int st = rep_decide_warp(sp, a, P, cap, mine_s, w, deplag, init, vbudget[t], 0ull, &nd,
-                                   lim, widx);
+                                   lim, widx, vbudget[t]);
     if (lane == 0) {
       vstatus[t] = st;
       vnodes[t] = nd;
