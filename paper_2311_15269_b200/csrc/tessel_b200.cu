@@ -101,6 +101,25 @@ struct DevFree {
   }
 };
 
+// Stream-ordered (de)allocation for buffers that grow while other streams
+// run: cudaFree synchronises the whole device, which would serialise the
+// asynchronous verification slots behind every buffer growth; the pool's
+// release threshold keeps freed memory cached.
+static void dev_grow(void **p, size_t bytes, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  if (*p) CK(cudaFreeAsync(*p, s));
+  *p = nullptr;
+  CK(cudaMallocAsync(p, bytes, s));
+}
+
 static void require_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -997,10 +1016,8 @@ struct DecideCtx {
 
   char *reserve(size_t bytes) {
     if (bytes > cap) {
-      if (buf) CK(cudaFree(buf));
-      buf = nullptr;
       size_t want = std::max(bytes, cap * 2);
-      CK(cudaMalloc(&buf, want));
+      dev_grow((void **)&buf, want, stream);
       cap = want;
     }
     return buf;
@@ -1238,6 +1255,8 @@ struct tsl_engine {
   int *d_sat_next = nullptr;
   int *d_gather = nullptr;
   size_t d_gather_cap = 0;
+  int *d_stash_idx = nullptr;  // window indices of the rows being stashed
+  size_t stash_idx_cap = 0;
   char *d_verify = nullptr;
   size_t d_verify_cap = 0;
   // asynchronous verification slots (windows in flight while the next one
@@ -1310,13 +1329,11 @@ struct tsl_engine {
     if (d_nr == n_r) return;
     host_tables(n_r);
     if (h_cnt.size() > d_cnt_cap) {
-      if (d_cnt) CK(cudaFree(d_cnt));
-      CK(cudaMalloc(&d_cnt, h_cnt.size() * sizeof(unsigned long long)));
+      dev_grow((void **)&d_cnt, h_cnt.size() * sizeof(unsigned long long), stream);
       d_cnt_cap = h_cnt.size();
     }
     if (h_off.size() > d_off_cap) {
-      if (d_off) CK(cudaFree(d_off));
-      CK(cudaMalloc(&d_off, h_off.size() * sizeof(long long)));
+      dev_grow((void **)&d_off, h_off.size() * sizeof(long long), stream);
       d_off_cap = h_off.size();
     }
     h2d(d_cnt, h_cnt.data(), h_cnt.size() * sizeof(unsigned long long), stream);
@@ -1327,20 +1344,16 @@ struct tsl_engine {
 
   void ensure_window(long long w) {
     if (w <= W_cap) return;
-    for (void *p : {(void *)d_assign, (void *)d_gate, (void *)d_act[0], (void *)d_act[1],
-                    (void *)d_sat_widx, (void *)d_sat_starts, (void *)d_def[0],
-                    (void *)d_def[1], (void *)d_surv})
-      if (p) CK(cudaFree(p));
     const int K = pool[R_K];
-    CK(cudaMalloc(&d_assign, (size_t)w * K));
-    CK(cudaMalloc(&d_gate, (size_t)w));
-    CK(cudaMalloc(&d_act[0], (size_t)w * sizeof(int)));
-    CK(cudaMalloc(&d_act[1], (size_t)w * sizeof(int)));
-    CK(cudaMalloc(&d_def[0], (size_t)w * sizeof(int)));
-    CK(cudaMalloc(&d_def[1], (size_t)w * sizeof(int)));
-    CK(cudaMalloc(&d_surv, (size_t)w * sizeof(int)));
-    CK(cudaMalloc(&d_sat_widx, (size_t)w * sizeof(int)));
-    CK(cudaMalloc(&d_sat_starts, (size_t)w * K * sizeof(int)));
+    dev_grow((void **)&d_assign, (size_t)w * K, stream);
+    dev_grow((void **)&d_gate, (size_t)w, stream);
+    dev_grow((void **)&d_act[0], (size_t)w * sizeof(int), stream);
+    dev_grow((void **)&d_act[1], (size_t)w * sizeof(int), stream);
+    dev_grow((void **)&d_def[0], (size_t)w * sizeof(int), stream);
+    dev_grow((void **)&d_def[1], (size_t)w * sizeof(int), stream);
+    dev_grow((void **)&d_surv, (size_t)w * sizeof(int), stream);
+    dev_grow((void **)&d_sat_widx, (size_t)w * sizeof(int), stream);
+    dev_grow((void **)&d_sat_starts, (size_t)w * K * sizeof(int), stream);
     W_cap = w;
   }
 
@@ -1350,7 +1363,7 @@ struct tsl_engine {
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
                     (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather,
                     (void *)d_def[0], (void *)d_def[1], (void *)d_verify, (void *)d_surv,
-                    (void *)d_sat_key, (void *)d_sat_next})
+                    (void *)d_sat_key, (void *)d_sat_next, (void *)d_stash_idx})
       if (p) cudaFree(p);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -1817,8 +1830,7 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
   const size_t b_lim = ((size_t)nlev * sizeof(int) + 255) / 256 * 256;
   const size_t need = 3 * b_i + 2 * b_l + b_lim + (size_t)count * K * sizeof(int);
   if (need > e->d_verify_cap) {
-    if (e->d_verify) CK(cudaFree(e->d_verify));
-    CK(cudaMalloc(&e->d_verify, need));
+    dev_grow((void **)&e->d_verify, need, e->stream);
     e->d_verify_cap = need;
   }
   char *q = e->d_verify;
@@ -1872,8 +1884,7 @@ int tsl_engine_verify_stash(tsl_engine *e, int slot, int64_t count, const int64_
   const int K = e->pool[R_K];
   const size_t need = (size_t)std::max<int64_t>(count, 1) * K;
   if (need > vs.rows_cap) {
-    if (vs.rows) CK(cudaFree(vs.rows));
-    CK(cudaMalloc(&vs.rows, need));
+    dev_grow((void **)&vs.rows, need, e->stream);  // written by k_stash_rows on e->stream
     vs.rows_cap = need;
   }
   vs.n_rows = count;
@@ -1883,10 +1894,11 @@ int tsl_engine_verify_stash(tsl_engine *e, int slot, int64_t count, const int64_
       if (widx[i] < 0 || widx[i] >= e->W) throw tsl::Error(TSL_EINVAL, "stash: bad window index");
       w32[i] = (int)widx[i];
     }
-    int *d_w = nullptr;
-    CK(cudaMalloc(&d_w, count * sizeof(int)));
-    DevFree guard;
-    guard.add(d_w);
+    if ((size_t)count > e->stash_idx_cap) {
+      dev_grow((void **)&e->d_stash_idx, (size_t)count * sizeof(int), e->stream);
+      e->stash_idx_cap = (size_t)count;
+    }
+    int *d_w = e->d_stash_idx;
     h2d(d_w, w32.data(), count * sizeof(int), e->stream);
     const long long total = count * K;
     COUNT_LAUNCH();
@@ -1929,8 +1941,7 @@ int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64
   const size_t need = 4 * b_i + 2 * b_l + b_lim + (size_t)count * K * sizeof(int);
   CK(cudaStreamSynchronize(vs.st));
   if (need > vs.cap) {
-    if (vs.buf) CK(cudaFree(vs.buf));
-    CK(cudaMalloc(&vs.buf, need));
+    dev_grow((void **)&vs.buf, need, vs.st);
     vs.cap = need;
   }
   char *q = vs.buf;
@@ -2044,8 +2055,7 @@ int tsl_engine_sat_rows(tsl_engine *e, int64_t first, int64_t count, int64_t *wi
   const int K = e->pool[R_K];
   const size_t need = (size_t)count * (K + 1);
   if (need > e->d_gather_cap) {
-    if (e->d_gather) CK(cudaFree(e->d_gather));
-    CK(cudaMalloc(&e->d_gather, need * sizeof(int)));
+    dev_grow((void **)&e->d_gather, need * sizeof(int), e->stream);
     e->d_gather_cap = need;
   }
   int *d_pos = e->d_gather, *d_out = e->d_gather + count;
