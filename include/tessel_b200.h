@@ -166,7 +166,7 @@ int tsl_engine_add_active(tsl_engine *e, int64_t count, const int64_t *widx);
  * that slot on the slot's own stream — it runs while later windows are
  * staged and scanned, concurrently with the other slots — and wait for /
  * read its results (same meaning as tsl_engine_verify). */
-#define TSL_VERIFY_SLOTS 4
+#define TSL_VERIFY_SLOTS 8
 int tsl_engine_verify_stash(tsl_engine *e, int slot, int64_t count, const int64_t *widx);
 int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64_t *pos,
                              const int64_t *widx, const int32_t *period,

@@ -35,10 +35,10 @@ from . import _native
 from .placement import PlacementSpec
 from .repetend import PROBE_NODES, lower_bound
 
-WINDOW_FIRST = 2048
+WINDOW_FIRST = int(os.environ.get("TESSEL_WINDOW_FIRST", "2048"))
 WINDOW_GROWTH = 4
 WINDOW_MAX = 1 << 21
-VERIFY_SLOTS = 4      # asynchronous verification slots (TSL_VERIFY_SLOTS)
+VERIFY_SLOTS = 8      # asynchronous verification slots (TSL_VERIFY_SLOTS)
 SAT_CHUNK = 1        # SAT rows returned with a level (the rest: device argmin walk)
 SMALL_BUDGET = 64     # first-pass RX-DFS nodes per probe (thread per probe) before deferral
 # node cap of the concurrent verify pass; longer probes run one at a time
