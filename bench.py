@@ -301,6 +301,7 @@ def run_b200_arm(args):
              "dj_nodes": 0, "verified": 0}
     phase = {"repetend": 0.0, "warmup": 0.0, "cooldown": 0.0}
     c = eng.counters
+    sp0 = _native.sp_stats()  # subtree-parallel completion decides (host-timed rounds)
 
     def check(res):
         nonlocal parity
@@ -335,6 +336,7 @@ def run_b200_arm(args):
                 phase[k] += res.report.phase_secs[k]
             check(res)
         c1 = _native.counters()
+        sp1 = _native.sp_stats()
         # (2) e2e: the public API from host objects — PlacementSpec in,
         # Schedule out, a fresh engine per step (placement tables uploaded,
         # count tables built), every host<->device copy inside the timed region
@@ -393,6 +395,9 @@ def run_b200_arm(args):
                   "dj_nodes_per_s": stats["dj_nodes"] / wall},
         "phase_s_per_step": {k: v / args.steps for k, v in phase.items()},
         "engine_kernel_s_per_step": kernel_s / args.steps,
+        "completion_sp_per_step": {
+            k: (sp1.get(k, 0) - sp0.get(k, 0)) / args.steps
+            for k in ("master_ms", "task_ms", "master_nodes", "tasks", "rounds")},
         "clocks": clocks,
         "roofline": _roofline(per_kernel, args.steps, args.workload),
     }
