@@ -28,7 +28,8 @@ from .placement import BlockInstance, PlacementSpec
 from .repetend import (Repetend, RepetendOutcome, entry_memory, lower_bound, make_repetend,
                        steady_memory_ok)
 from .schedule import RepetendInfo, Schedule
-from .solver import (SolveRequest, SolveStats, Status, default_budget, solve_decide,
+from . import _core
+from .solver import (Lowering, SolveRequest, SolveStats, Status, default_budget, solve_decide,
                      solve_min_makespan)
 
 DEFAULT_MAX_NR = 8
@@ -203,20 +204,36 @@ def _budget_left(deadline: float) -> float:
 def _completion_feasible(p: PlacementSpec, rep: Repetend, cap: Optional[int], deadline: float,
                          report: SearchReport) -> bool:
     """Lazy check: warmup and cooldown each decidable within the serial
-    horizon under a 2M-node cap (completion.py:156-182)."""
+    horizon under a 2M-node cap (completion.py:156-182).  Both decides run in
+    one batched launch; the cooldown's outcome and statistics only count when
+    the warmup is SAT, as in the reference's sequential evaluation."""
     phases = (
         (warmup_blocks(rep), (0,) * p.num_devices),
         (cooldown_blocks(rep),
          tuple(max(0, v) for v in cooldown_entry_memory(p, rep, rep.n_r))),
     )
+    probs = []  # per phase: the decide problem, or None (empty phase / bounds refute)
     for insts, init in phases:
         if not insts:
+            probs.append("empty")
             continue
         horizon = sum(p.block(b.stage).time_cost for b in insts)
-        req = SolveRequest(p, tuple(sorted(insts)), init, cap, horizon, "decide")
-        res = solve_decide(req, budget=_budget_left(deadline), probe_nodes=LAZY_CHECK_NODES)
-        report.stats.merge(res.stats)
-        if res.status != Status.SATISFIABLE:
+        low = Lowering(SolveRequest(p, tuple(sorted(insts)), init, cap, horizon, "decide"))
+        probs.append(low.problem(horizon, LAZY_CHECK_NODES))
+    batch = [q for q in probs if isinstance(q, dict)]
+    t0 = time.monotonic()
+    outs = iter(_core.decide_batch(batch, deadline) if batch else [])
+    wall = time.monotonic() - t0
+    for q in probs:
+        if q == "empty":
+            continue
+        if q is None:  # a fixed block misses the horizon: UNSAT without a decide
+            return False
+        status, _, nodes = next(outs)
+        report.stats.decides += 1
+        report.stats.nodes += nodes
+        report.stats.wall_secs += wall / len(batch)
+        if status != _core.SAT:
             return False
     return True
 

@@ -196,3 +196,10 @@ def oracle_decide(n, dur, devmask, mem, edges, order, lo, hi, ndev, init_mem, ca
     """Stand-in for paper_2311_15269_b200._core.decide in CPU tests."""
     return oracle.decide(n, dur, devmask, mem, edges, order, lo, hi, ndev, init_mem, cap,
                          node_budget, 0.0)
+
+
+def oracle_decide_batch(problems, deadline=0.0):
+    """Stand-in for paper_2311_15269_b200._core.decide_batch in CPU tests."""
+    return [oracle.decide(p["n"], p["dur"], p["devmask"], p["mem"], p["edges"], p["order"],
+                          p["lo"], p["hi"], p["ndev"], p["init_mem"], p["cap"],
+                          p.get("node_budget", 0), 0.0) for p in problems]

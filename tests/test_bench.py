@@ -27,8 +27,9 @@ if os.environ.get("TESSEL_BENCH_CPU_SHIM") == "1":
     sys.path.insert(0, os.path.join(os.environ["TESSEL_REPO"], "tests"))
     import paper_2311_15269_b200._core as core
     import paper_2311_15269_b200.engine as E
-    from cpu_engine import OracleEngine, oracle_decide
+    from cpu_engine import OracleEngine, oracle_decide, oracle_decide_batch
     core.decide = oracle_decide
+    core.decide_batch = oracle_decide_batch
     _init = E.BatchedRepetendSearch.__init__
     def _patched(self, p, device=0, native=None):
         _init(self, p, device, native if native is not None else OracleEngine(p))

@@ -24,11 +24,12 @@ CASES = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "k4_k3", "m4_cap8", "C1",
 
 
 def _patch_decide(monkeypatch):
-    from cpu_engine import oracle_decide
+    from cpu_engine import oracle_decide, oracle_decide_batch
 
     import paper_2311_15269_b200._core as core
 
     monkeypatch.setattr(core, "decide", oracle_decide)
+    monkeypatch.setattr(core, "decide_batch", oracle_decide_batch)
 
 
 def _run(name, comm=None, small_windows=False, speculate=True, repair=True, stage=8):
@@ -132,10 +133,11 @@ def _worker(rank, world, port, names, out_dir):
                             world_size=world)
     try:
         import paper_2311_15269_b200._core as core
-        from cpu_engine import oracle_decide
+        from cpu_engine import oracle_decide, oracle_decide_batch
         from paper_2311_15269_b200.parallel import Comm
 
         core.decide = oracle_decide
+        core.decide_batch = oracle_decide_batch
         comm = Comm()
         for name in names:
             for small in (False, True):
