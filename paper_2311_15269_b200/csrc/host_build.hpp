@@ -373,6 +373,27 @@ inline std::vector<int> rep_build(const Placement &pl) {
   put(R_FR, fr);
   put(R_DPPTR, dp_ptr);
   put(R_DP, dp);
+  {  // chunk item masks for wdj_propagate (u64 as two ints)
+    const int nrc = (m + 31) / 32, npc = ((int)pairx.size() + 31) / 32;
+    std::vector<int> rowcm(2 * (nrc > 0 ? nrc : 1), 0), paircm(2 * (npc > 0 ? npc : 1), 0);
+    auto setc = [&](std::vector<int> &v, int c, int item) {
+      if (K > 64) {
+        v[2 * c] = v[2 * c + 1] = -1;
+      } else {
+        v[2 * c + (item >> 5)] |= (int)(1u << (item & 31));
+      }
+    };
+    for (int r = 0; r < m; ++r) {
+      setc(rowcm, r / 32, rsrc[r]);
+      setc(rowcm, r / 32, rdst[r]);
+    }
+    for (size_t q = 0; q < pairx.size(); ++q) {
+      setc(paircm, (int)q / 32, pairx[q]);
+      setc(paircm, (int)q / 32, pairy[q]);
+    }
+    put(R_ROWCM, rowcm);
+    put(R_PAIRCM, paircm);
+  }
   put(R_INTWIN, in_twins(out_ptr, out_dst, in_ptr, in_src, K));
   {  // wrr_dfs.cuh tables (u64 masks as two ints, low word first)
     const bool fits = K <= 64 && D <= 64;

@@ -120,6 +120,10 @@ enum {
   R_SUCCM, R_PREDM, R_CONFM, R_DEVM, R_DEVITM, R_MULTI, R_WINB, R_WRR,
   // 1: repetend probes run the strong search first (wst_dfs.cuh)
   R_WST,
+  // per 32-row chunk of the edge rows / of the disjunctive pairs: the items
+  // they touch (u64, all ones when K > 64) — wdj_propagate skips chunks
+  // none of whose items changed
+  R_ROWCM, R_PAIRCM,
   R_WORDS, R_HDR
 };
 

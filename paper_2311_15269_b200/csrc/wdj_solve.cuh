@@ -65,35 +65,55 @@ __device__ inline WdjWs wdj_carve(int *smem, int *gsnap, int K, int npair) {
 
 struct WdjCtx {
   const int *rsrc, *rdst, *rbase, *pairx, *pairy, *dur, *mem, *dpptr, *dp, *devptr, *devitems;
-  const int *init;
+  const int *init, *rowcm, *paircm;
   int K, D, m, ndep, npair, nw, P, cap;
 };
+
+__device__ __forceinline__ unsigned long long wdj_u64(const int *p) {
+  return (unsigned long long)(unsigned)p[0] | ((unsigned long long)(unsigned)p[1] << 32);
+}
+__device__ __forceinline__ unsigned long long wdj_ibit(int i) {
+  return i < 64 ? 1ull << i : ~0ull;
+}
 
 __device__ __forceinline__ bool wdj_bit(const unsigned *b, int q) {
   return (b[q >> 5] >> (q & 31)) & 1u;
 }
 
-// Propagate to a fixpoint of the sound rules; false = infeasible.
-__device__ inline bool wdj_propagate(const WdjCtx &c, WdjWs &w) {
+// Propagate to a fixpoint of the sound rules; false = infeasible.  `cur`:
+// the items whose bounds or pair orientations changed since the last
+// fixpoint (all at the root, the branched pair's two items after an
+// orientation); each round relaxes only the 32-row / 32-pair chunks that
+// touch a changed item (R_ROWCM / R_PAIRCM) — a row or pair none of whose
+// items changed cannot change anything — and collects the items it changed
+// for the next round.
+__device__ inline bool wdj_propagate(const WdjCtx &c, WdjWs &w, unsigned long long cur) {
   const int lane = wrx_lane();
   int quiet = 0;  // rounds since the last new orientation
   for (;;) {
-    bool changed = false, oriented = false, fail = false;
-    for (int r = lane; r < c.m; r += 32) {
+    bool oriented = false, fail = false;
+    unsigned long long mine = 0;
+    for (int base = 0; base < c.m; base += 32) {
+      if (!(wdj_u64(c.rowcm + 2 * (base >> 5)) & cur)) continue;
+      const int r = base + lane;
+      if (r >= c.m) continue;
       const int s = c.rsrc[r], d = c.rdst[r];
       const int lag = c.rbase[r] - (r < c.ndep ? w.av[s] - w.av[d] : 1) * c.P;
       const int nl = w.lo[s] + lag;
       if (nl > w.lo[d]) {
         atomicMax(&w.lo[d], nl);
-        changed = true;
+        mine |= wdj_ibit(d);
       }
       const int nh = w.hi[d] - lag;
       if (nh < w.hi[s]) {
         atomicMin(&w.hi[s], nh);
-        changed = true;
+        mine |= wdj_ibit(s);
       }
     }
-    for (int q = lane; q < c.npair; q += 32) {
+    for (int base = 0; base < c.npair; base += 32) {
+      if (!(wdj_u64(c.paircm + 2 * (base >> 5)) & cur)) continue;
+      const int q = base + lane;
+      if (q >= c.npair) continue;
       const int x = c.pairx[q], y = c.pairy[q];
       bool xf = wdj_bit(w.ox, q), yf = wdj_bit(w.oy, q);
       if (!xf && !yf) {
@@ -113,19 +133,21 @@ __device__ inline bool wdj_propagate(const WdjCtx &c, WdjWs &w) {
       const int nl = w.lo[a] + c.dur[a];
       if (nl > w.lo[b]) {
         atomicMax(&w.lo[b], nl);
-        changed = true;
+        mine |= wdj_ibit(b);
       }
       const int nh = w.hi[b] - c.dur[a];
       if (nh < w.hi[a]) {
         atomicMin(&w.hi[a], nh);
-        changed = true;
+        mine |= wdj_ibit(a);
       }
     }
     __syncwarp();
     for (int i = lane; i < c.K; i += 32) fail |= w.lo[i] > w.hi[i];
     if (__any_sync(WRX_FULL, fail)) return false;
     const bool any_or = __any_sync(WRX_FULL, oriented);
-    if (!__any_sync(WRX_FULL, changed) && !any_or) return true;
+    cur = (unsigned long long)__reduce_or_sync(WRX_FULL, (unsigned)mine) |
+          ((unsigned long long)__reduce_or_sync(WRX_FULL, (unsigned)(mine >> 32)) << 32);
+    if (!cur && !any_or) return true;
     quiet = any_or ? 0 : quiet + 1;
     if (quiet > c.K + 1) return false;  // positive cycle in a fixed difference system
   }
@@ -216,6 +238,8 @@ __device__ inline int wdj_decide(const int *pool, int P, int cap, const int *ini
   c.devptr = pool + pool[R_DEVPTR];
   c.devitems = pool + pool[R_DEVITEMS];
   c.init = init;
+  c.rowcm = pool + pool[R_ROWCM];
+  c.paircm = pool + pool[R_PAIRCM];
   *nodes_out = 0;
   for (int i = lane; i < c.nw; i += 32) w.ox[i] = w.oy[i] = 0u;
   __syncwarp();
@@ -224,7 +248,7 @@ __device__ inline int wdj_decide(const int *pool, int P, int cap, const int *ini
     for (int d = lane; d < c.D; d += 32) bad |= init[d] > cap;
     if (__any_sync(WRX_FULL, bad)) return DJ_UNSAT;
   }
-  if (!wdj_propagate(c, w) || !wdj_mem_ok(c, w)) return DJ_UNSAT;
+  if (!wdj_propagate(c, w, ~0ull) || !wdj_mem_ok(c, w)) return DJ_UNSAT;
   long long nodes = 0;
   int depth = 0;
   bool descend = true;
@@ -283,7 +307,7 @@ __device__ inline int wdj_decide(const int *pool, int P, int cap, const int *ini
       *nodes_out = nodes;
       return DJ_UNKNOWN;
     }
-    if (wdj_propagate(c, w) && wdj_mem_ok(c, w)) {
+    if (wdj_propagate(c, w, wdj_ibit(c.pairx[pid]) | wdj_ibit(c.pairy[pid])) && wdj_mem_ok(c, w)) {
       ++depth;
       descend = true;
     }
