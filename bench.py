@@ -52,7 +52,8 @@ METRIC = BASE["metric"]
 UNIT = "candidates/s"
 DEFAULT_WORKLOAD = "C2@8"
 GOLDEN = {"C2@8": "C2_8", "C2@4": "C2_4", "C2@3": "C2_3", "C1": "C1", "C3@9": "C3_9", "C5@2": "C5_2",
-          "C5@3": "C5_3", "C4b": "C4b", "C3@12": "C3_12", "C4a@3": "C4a_3", "C4a@4": "C4a_4"}
+          "C5@3": "C5_3", "C4b": "C4b", "C3@12": "C3_12", "C4a@3": "C4a_3", "C4a@4": "C4a_4",
+          "C5@4": "C5_4", "C5@5": "C5_5"}
 
 
 def _env_rank():

@@ -127,9 +127,11 @@ FAST = ["v4_unit_cap4", "v4_demo_cap4", "x4_demo_k3", "m4_cap8", "k4_k3", "v2_k4
         "C1", "C2_3", "C3_9", "C5_2",
         # the full-size parity configs — seconds each on the B200
         "C2_4", "C3_12", "C4a_3", "C4a_4", "C4b", "C5_3",
-        # BASELINE configs[4] (K16) at N_R <= 4: reference golden from
-        # tests/golden/make_par_golden.py (the reference's own functions)
-        "C5_4",
+        # BASELINE configs[4] (K16) at N_R <= 4 and <= 5 (9.4 M candidates):
+        # reference goldens from tests/golden/make_par_golden.py (the
+        # reference's own functions, sequential-equivalent, 13.6 min and
+        # 3.7 h on the CPU container's cores)
+        "C5_4", "C5_5",
         # eager completion (completion.py:359-368) and the entry-memory gate
         "eager_C1", "eager_C2_3", "eager_C3_9", "eager_m4_cap8", "eager_x4_demo_k3",
         "eager_v4_demo_cap4", "gate_pairs_a_cap4", "gate_pairs_b_cap3", "gate_pairs_c_cap5"]
