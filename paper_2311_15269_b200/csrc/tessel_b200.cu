@@ -554,7 +554,8 @@ __global__ void __launch_bounds__(128, RESOLVE_MIN_BLOCKS) k_resolve_warp(const 
                                                       long long widx_limit,
                                                       unsigned long long budget_ns,
                                                       int *ws_base, long long ws_words,
-                                                      int *dev_limit, int dj_warp) {
+                                                      int *dev_limit, int dj_warp,
+                                                      int *work) {
   extern __shared__ int sp[];
   // n_def_dev: device-side count (k_root survivors; probes counted there)
   if (n_def_dev) n_def = *n_def_dev;
@@ -593,7 +594,17 @@ __global__ void __launch_bounds__(128, RESOLVE_MIN_BLOCKS) k_resolve_warp(const 
     }
     __syncwarp();
   };
-  for (long long t = gw; t < n_def; t += nwarps) {
+  // work: the launch's probe counter — each warp takes the next probe when it
+  // is done with one (probe costs are heavy-tailed: a static stride leaves
+  // most warps idle behind a few long ones); nullptr = static stride
+  long long t_static = gw - nwarps;
+  auto next = [&]() -> long long {
+    if (!work) return t_static += nwarps;
+    int v = 0;
+    if (lane == 0) v = atomicAdd(work, 1);
+    return (long long)__shfl_sync(WRX_FULL, v, 0);
+  };
+  for (long long t = next(); t < n_def; t = next()) {
     const int widx = def_in[t];
     if (widx > widx_limit) continue;
     if (spec_retired(widx)) {
@@ -1071,6 +1082,13 @@ bool dj_mode_warp(const int *pool) {
 bool dj_split() {
   const char *m = getenv("TSL_DJ_SPLIT");
   return m && std::string(m) == "1";
+}
+
+// TSL_RESOLVE_DYN=0 restores the static grid stride of k_resolve_warp
+// (default: probes handed out one at a time through a launch counter)
+bool resolve_dynamic() {
+  const char *m = getenv("TSL_RESOLVE_DYN");
+  return !(m && std::string(m) == "0");
 }
 
 bool decide_mode_warp() {
@@ -1588,7 +1606,7 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
   const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
   const long long n_in = e->n_act;
   {
-    const int init[5] = {0, 0, 0, 0, (int)std::min<int64_t>(widx_limit, 0x7fffffff)};
+    const int init[6] = {0, 0, 0, 0, (int)std::min<int64_t>(widx_limit, 0x7fffffff), 0};
     h2d(e->d_counters, init, sizeof init, e->stream);
   }
   CK(cudaMemsetAsync(e->d_stats, 0, 8 * sizeof(unsigned long long), e->stream));
@@ -1641,7 +1659,8 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
     COUNT_LAUNCH();
     k_resolve_warp<<<(int)sblocks, 32 * swpb, ssmem, e->stream>>>(
         e->d_pool, e->d_assign, e->d_surv, 0, e->d_counters + 3, o, period, full, stage, 0,
-        icap, widx_limit, budget_ns, e->d_ws, e->ws_words, e->d_counters + 4, 0);
+        icap, widx_limit, budget_ns, e->d_ws, e->ws_words, e->d_counters + 4, 0,
+        resolve_dynamic() ? e->d_counters + 5 : nullptr);
     CK(cudaGetLastError());
   } else if (n_in > 0) {
     COUNT_LAUNCH();
@@ -1681,9 +1700,9 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
   const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
   const long long n_def = e->n_def;
   // continue appending to the level's SAT list and to the active list
-  int counters[5] = {(int)e->n_act, (int)e->n_sat, 0, 0,
-                     (int)std::min<int64_t>(widx_limit, 0x7fffffff)};
-  h2d(e->d_counters, counters, 5 * sizeof(int), e->stream);
+  int counters[6] = {(int)e->n_act, (int)e->n_sat, 0, 0,
+                     (int)std::min<int64_t>(widx_limit, 0x7fffffff), 0};
+  h2d(e->d_counters, counters, 6 * sizeof(int), e->stream);
   CK(cudaMemsetAsync(e->d_stats, 0, 8 * sizeof(unsigned long long), e->stream));
   const int threads = 128;
   long long blocks = (n_def + threads - 1) / threads;
@@ -1738,7 +1757,8 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
         e->d_pool, e->d_assign, rx_in, (int)n_def, rx_count, o, period,
         node_budget < 0 ? 0 : node_budget, stage_budget < 0 ? -1 : stage_budget,
         dj_budget < 0 ? 0 : dj_budget, icap, widx_limit, budget_ns, e->d_ws, e->ws_words,
-        e->d_counters + 4, dj_mode_warp(e->pool.data()) ? 1 : 0);
+        e->d_counters + 4, dj_mode_warp(e->pool.data()) ? 1 : 0,
+        resolve_dynamic() ? e->d_counters + 5 : nullptr);
     CK(cudaGetLastError());
   } else if (n_def > 0) {
     COUNT_LAUNCH();

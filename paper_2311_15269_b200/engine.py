@@ -103,7 +103,8 @@ class EngineCounters:
         else:
             self.resolve_ms += ms
         if TRACE and tag is not None:
-            self.trace.append((*tag, round(ms, 3), {k: v for k, v in st.items() if v}))
+            self.trace.append((*tag, round(ms, 3), {**{k: v for k, v in st.items() if v},
+                                                     "t": round(time.perf_counter(), 4)}))
         self.levels += level
         self.launches += 1
         for k in ("probes", "root_refuted", "nodes", "capped", "sat", "deferred", "dj_refuted",
@@ -251,6 +252,10 @@ class BatchedRepetendSearch:
         bud = [0 if q == self.lb else PROBE_NODES for q in per]
         run_bud = [VERIFY_FIRST if (b == 0 or b > VERIFY_FIRST) else b for b in bud]
         self.eng.verify_launch(job.slot, positions, w, per, run_bud, cap)
+        if TRACE:
+            self.counters.trace.append((n_r, r0, 0, "vlaunch", 0.0,
+                                        {"n": len(w), "slot": job.slot,
+                                         "t": round(time.perf_counter(), 4)}))
 
     def finish_window(self, job: "WindowJob", feasible) -> WindowResult:
         n_r, r0, r1, cap, bound, deadline = job.args
