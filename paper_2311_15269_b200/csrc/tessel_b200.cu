@@ -760,7 +760,8 @@ __global__ void __launch_bounds__(128, 1) k_verify_warp(const int *__restrict__ 
                                                      long long *vnodes, int *vstarts,
                                                      int *vlim, int pmin, int nlev,
                                                      const unsigned char *__restrict__ rows,
-                                                     const int *__restrict__ vpos) {
+                                                     const int *__restrict__ vpos,
+                                                     int cancel) {
   extern __shared__ int sp[];
   load_pool(sp, gpool);
   const int K = sp[R_K];
@@ -777,9 +778,11 @@ __global__ void __launch_bounds__(128, 1) k_verify_warp(const int *__restrict__ 
     const int P = vper[t], widx = vwidx[t];
     // per-period speculative retirement: a SAT (w, P) retires (w2, P2) with
     // w2 > w and P2 >= P if its completion check passes (the host decides)
+    // (cancel = 0: every probe of the launch is resident at once, so a
+    // cancelled one would only be re-run later, on the critical path)
     int *lim = vlim + (P - pmin);
-    int l = 0;
-    if (lane == 0) l = *(volatile int *)lim;
+    int l = 0x7fffffff;
+    if (cancel && lane == 0) l = *(volatile int *)lim;
     l = __shfl_sync(WRX_FULL, l, 0);
     if (widx > l) {
       if (lane == 0) {
@@ -793,7 +796,7 @@ __global__ void __launch_bounds__(128, 1) k_verify_warp(const int *__restrict__ 
     const unsigned char *a = rows ? rows + (long long)vpos[t] * K : assign + (long long)widx * K;
     long long nd = 0;
     const int st = rep_decide_warp(sp, a, P, cap, mine_s, w, deplag, init, vbudget[t], 0ull, &nd,
-                                   lim, widx, vbudget[t]);
+                                   cancel ? lim : nullptr, widx, vbudget[t]);
     if (lane == 0) {
       vstatus[t] = st;
       vnodes[t] = nd;
@@ -1822,6 +1825,20 @@ int tsl_engine_add_active(tsl_engine *e, int64_t count, const int64_t *widx) {
   API_END
 }
 
+// Whether a verification launch lets a SAT cancel the higher probes it may
+// retire: only when the launch's warps cannot all be resident at once
+// (cancelling then frees a warp slot for a waiting probe); a resident probe
+// runs on (an aborted one would be re-run after the launch, adding its whole
+// count to the window's critical path).  TSL_VERIFY_CANCEL=1 / 0 forces it.
+static int verify_cancel(tsl_engine *e, long long count, int wpb, size_t smem) {
+  const char *m = getenv("TSL_VERIFY_CANCEL");
+  if (m && std::string(m) == "1") return 1;
+  if (m && std::string(m) == "0") return 0;
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_warp, 32 * wpb, smem));
+  return count > (long long)std::max(per_sm, 1) * e->num_sms * wpb ? 1 : 0;
+}
+
 int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const int32_t *period,
                       const int64_t *node_budget, int64_t cap, int32_t *status_out,
                       int64_t *nodes_out, int32_t *starts_out) {
@@ -1877,12 +1894,13 @@ int tsl_engine_verify(tsl_engine *e, int64_t count, const int64_t *widx, const i
                             (int)smem));
   long long blocks = (count + wpb - 1) / wpb;
   blocks = std::min<long long>(blocks, (long long)e->num_sms * 16);
+  const int cancel = verify_cancel(e, count, wpb, smem);
   CK(cudaEventRecord(e->ev0, e->stream));
   COUNT_LAUNCH();
   k_verify_warp<<<(int)blocks, 32 * wpb, smem, e->stream>>>(e->d_pool, e->d_assign, d_w, d_p,
                                                              d_b, (int)count, icap, d_st, d_n,
                                                              d_s, d_lim, pmin, nlev, nullptr,
-                                                             nullptr);
+                                                             nullptr, cancel);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e->ev1, e->stream));
   d2h(status_out, d_st, count * sizeof(int), e->stream);
@@ -1989,11 +2007,12 @@ int tsl_engine_verify_launch(tsl_engine *e, int slot, int64_t count, const int64
     CK(cudaFuncSetAttribute(k_verify_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
   long long blocks = std::min<long long>((count + wpb - 1) / wpb, (long long)e->num_sms * 16);
+  const int cancel = verify_cancel(e, count, wpb, smem);
   CK(cudaEventRecord(vs.ev0, vs.st));
   COUNT_LAUNCH();
   k_verify_warp<<<(int)blocks, 32 * wpb, smem, vs.st>>>(
       e->d_pool, e->d_assign, d_w, d_p, d_b, (int)count, icap, vs.d_st, vs.d_n, vs.d_s, d_lim,
-      pmin, nlev, vs.rows, d_pos);
+      pmin, nlev, vs.rows, d_pos, cancel);
   CK(cudaGetLastError());
   CK(cudaEventRecord(vs.ev1, vs.st));
   return TSL_OK;
