@@ -58,15 +58,26 @@ RESOLVE_STAGES = ((DJ_BUDGET, 32_768), (0, 0))
 SPEC_STAGES = ((DJ_BUDGET, int(os.environ.get("TESSEL_SPEC_STAGE", "65536"))),)
 
 
+# latency mode of the speculative resolve stage: a level with few deferred
+# probes (< SPEC_SMALL_NDEF, all resident at once) is bound by its longest
+# probe's stage budget, so its DFS stage stops after SPEC_SMALL nodes and the
+# rest goes to the window-end verification, which overlaps the next levels;
+# a level with many deferred probes keeps the full stage budget (throughput:
+# its early SATs retire the higher candidates)
+SPEC_SMALL = int(os.environ.get("TESSEL_SPEC_SMALL", "1024"))
+SPEC_SMALL_NDEF = int(os.environ.get("TESSEL_SPEC_SMALL_NDEF", "4096"))
+
+
 def spec_stages(k: int):
-    """The single resolve stage's DFS budget, sized for ~150 ms of warp DFS:
-    64k nodes when every stage fits one lane (K <= 32, ~2.5 us/node), 16k
-    when lanes carry two stages (~8 us/node; measured on C4a@3: 11.7 s vs
-    19.2 s with 64k — its deferred probes are mostly 400k-node TIMEOUTs that
-    the window-end verification settles in one launch)."""
+    """The single resolve stage's DFS budget: 64k nodes when every stage fits
+    one lane (K <= 32; cut to SPEC_SMALL on levels with few deferred probes),
+    SPEC_SMALL when lanes carry two stages (K > 32, ~3x dearer nodes: their
+    deferred probes are mostly 400k-node TIMEOUTs that the window-end
+    verification settles concurrently; measured with 16k / 1k nodes: C4a@3
+    4.5 / 3.0 s, C4a@4 5.3 / 3.6 s, C5@5 5.4 / 4.8 s)."""
     if "TESSEL_SPEC_STAGE" in os.environ:
         return SPEC_STAGES
-    return ((DJ_BUDGET, 65536 if k <= 32 else 16384),)
+    return ((DJ_BUDGET, 65536 if k <= 32 else SPEC_SMALL),)
 TRACE = os.environ.get("TESSEL_TRACE", "0") == "1"
 
 
@@ -460,6 +471,8 @@ class BatchedRepetendSearch:
             si, reruns = 0, 0
             while n_def and si < len(self.resolve_stages):
                 dj_budget, stage_budget = self.resolve_stages[si]
+                if self.speculate and 0 < SPEC_SMALL < stage_budget and n_def < SPEC_SMALL_NDEF:
+                    stage_budget = SPEC_SMALL
                 n_sat, widx, rows, n_act, n_def, st = self.eng.resolve(
                     period, node_cap, stage_budget, dj_budget, cap, limit, budget_secs,
                     SAT_CHUNK)
