@@ -21,6 +21,7 @@ from collections.abc import Sequence
 from dataclasses import dataclass, field
 from typing import Optional
 
+from .engine import TRACE as ENGINE_TRACE
 from .engine import (VERIFY_SLOTS, WINDOW_FIRST, WINDOW_GROWTH, WINDOW_MAX,
                      BatchedRepetendSearch)
 from .parallel import SoloComm, split_range
@@ -303,6 +304,7 @@ class _Feasibility:
     def __init__(self, p, cap, lazy, deadline):
         self.p, self.cap, self.lazy, self.deadline = p, cap, lazy, deadline
         self.memo: dict = {}
+        self.trace = None  # engine trace list (TESSEL_TRACE=1): one entry per evaluation
 
     def evaluate(self, rep: Repetend):
         # lazy checks depend on the assignment only (warmup / cooldown sets and
@@ -310,6 +312,7 @@ class _Feasibility:
         # witness, so it is keyed by the whole repetend
         key = rep.assignment if self.lazy else (rep.assignment, rep.internal, rep.period)
         if key not in self.memo:
+            t0 = time.perf_counter()
             scratch = SearchReport(0, 0, 0, self.lazy)
             ok, sched, exc = False, None, None
             try:
@@ -323,6 +326,10 @@ class _Feasibility:
             except CompletionTimeout as e:
                 exc = e
             self.memo[key] = (ok, sched, exc, scratch)
+            if self.trace is not None:
+                t1 = time.perf_counter()
+                self.trace.append((rep.n_r, 0, rep.period, "feasible", round((t1 - t0) * 1e3, 3),
+                                   {"ok": int(ok), "t": round(t1, 4)}))
         return self.memo[key]
 
     def ok(self, rep: Repetend) -> bool:
@@ -388,6 +395,8 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
     log = CandidateLog(p, cap, eng.unrank)
     report.candidates = log
     feas = _Feasibility(p, cap, lazy, deadline)
+    if ENGINE_TRACE:
+        feas.trace = eng.counters.trace
     k = p.num_stages
 
     def feasible(n_r, rank, period, starts):

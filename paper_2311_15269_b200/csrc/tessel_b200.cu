@@ -268,26 +268,109 @@ __device__ __forceinline__ void emit_sat(const ProbeOut &o, int widx, const int 
 // to k_probe's reference-exact DFS.
 __host__ __device__ inline int root_warp_words(const int *pool) {
   const int K = pool[R_K];
-  return ((wrx_state_words(K, pool[R_MAXDI]) + 3) & ~3) + ((K + 3) & ~3);
+  const int nmemb = pool[pool[R_DEVPTR] + pool[R_D]];  // device memberships
+  return ((wrx_state_words(K, pool[R_MAXDI]) + 3) & ~3) + ((K + 3) & ~3) +
+         3 * ((nmemb + 3) & ~3);
 }
 
-__global__ void __launch_bounds__(256) k_root(const int *__restrict__ gpool,
+// Root _dev_ok of every device at once (nothing placed: release a = lo,
+// deadline e = hi + dur), one lane per device membership p (dev_items order)
+// instead of one device after another: for p's device, the suffix (>= p in
+// the stable release order (a, p)) and prefix (<= p in the stable deadline
+// order (e, a, p)) sums of kernel_c.pyx:470-508 and the serial-completion
+// bound max(sum d, a + suffix d) <= max e.  ea / ee / ed: per-membership
+// scratch (3 x nmemb words).  ROOT_MEMB_CHUNKS x 32 memberships at most.
+#define ROOT_MEMB_CHUNKS 4
+#define ROOT_ROWS 9  // edge rows per lane held in registers by k_root (m <= 288)
+__device__ __forceinline__ bool root_devs_ok(const int *sp, const WWs &w, int *ea, int *ee,
+                                             int *ed, int nmemb, const int (&q0)[ROOT_MEMB_CHUNKS],
+                                             const int (&q1)[ROOT_MEMB_CHUNKS]) {
+  const int lane = threadIdx.x & 31;
+  const int *items = sp + sp[R_DEVITEMS], *dur = sp + sp[R_DUR];
+  for (int p = lane; p < nmemb; p += 32) {
+    const int it = items[p], du = dur[it];
+    ea[p] = w.lo[it];
+    ee[p] = w.hi[it] + du;
+    ed[p] = du;
+  }
+  __syncwarp();
+  bool bad = false;
+#pragma unroll
+  for (int c = 0; c < ROOT_MEMB_CHUNKS; ++c) {
+    const int p = 32 * c + lane;
+    if (32 * c >= nmemb) break;
+    if (p < nmemb) {
+      const int ai = ea[p], ei = ee[p];
+      int suf_d = 0, suf_e = -(1 << 30), pre_d = 0, pre_a = 1 << 30, lim = -(1 << 30), sd = 0;
+      for (int q = q0[c]; q < q1[c]; ++q) {
+        const int aj = ea[q], ej = ee[q], dj = ed[q];
+        lim = ej > lim ? ej : lim;
+        sd += dj;
+        const bool ge = aj > ai || (aj == ai && q >= p);
+        if (ge) {
+          suf_d += dj;
+          suf_e = ej > suf_e ? ej : suf_e;
+        }
+        if (ej < ei || (ej == ei && !(ge && q != p))) {
+          pre_d += dj;
+          pre_a = aj < pre_a ? aj : pre_a;
+        }
+      }
+      bad |= ai + suf_d > suf_e || pre_a + pre_d > ei || ai + suf_d > lim || sd > lim;
+    }
+  }
+  const bool ok = !__any_sync(WRX_FULL, bad);
+  __syncwarp();
+  return ok;
+}
+
+__global__ void __launch_bounds__(256, 3) k_root(const int *__restrict__ gpool,
                                               const unsigned char *__restrict__ assign,
                                               const int *__restrict__ act_in, int n_in,
                                               ProbeOut o, int *__restrict__ surv, int P, int cap,
-                                              long long widx_limit) {
+                                              long long widx_limit, int devs_serial) {
   extern __shared__ int sp[];
   load_pool(sp, gpool);
   const int K = sp[R_K], D = sp[R_D], m = sp[R_M], ndep = sp[R_NDEP];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int *mine = sp + ((sp[R_WORDS] + 3) & ~3) + wib * root_warp_words(sp);
   int *av = mine + ((wrx_state_words(K, sp[R_MAXDI]) + 3) & ~3);
+  const int nmemb = sp[sp[R_DEVPTR] + D];
+  int *ea = av + ((K + 3) & ~3), *ee = ea + ((nmemb + 3) & ~3), *ed = ee + ((nmemb + 3) & ~3);
   WWs w = wrx_carve(mine, nullptr, K, sp[R_MAXDI]);
   const int nw = (K + 31) / 32;
   for (int i = lane; i < nw; i += 32) w.placed[i] = 0u;
+  // this lane's memberships: their device's range in dev_items
+  const bool batched = nmemb <= 32 * ROOT_MEMB_CHUNKS && !devs_serial;
+  int q0[ROOT_MEMB_CHUNKS], q1[ROOT_MEMB_CHUNKS];
+#pragma unroll
+  for (int c = 0; c < ROOT_MEMB_CHUNKS; ++c) {
+    const int p = 32 * c + lane;
+    q0[c] = q1[c] = 0;
+    if (batched && p < nmemb)
+      for (int d = 0; d < D; ++d)
+        if (at_ptr(sp, R_DEVPTR, d) <= p && p < at_ptr(sp, R_DEVPTR, d + 1)) {
+          q0[c] = at_ptr(sp, R_DEVPTR, d);
+          q1[c] = at_ptr(sp, R_DEVPTR, d + 1);
+        }
+  }
   const int *rsrc = sp + sp[R_RSRC], *rdst = sp + sp[R_RDST], *rbase = sp + sp[R_RBASE];
   const int anchor = (K - 1) * (P + sp[R_MAXDUR]);
   const RepView v = rep_view(sp, P, cap, nullptr, nullptr);
+  // Register rows: lane l relaxes the contiguous block [l * per, l * per +
+  // per) of the m edge rows, lo forward and hi backward through the block
+  // (consecutive rows of a stage chain advance several hops per round
+  // instead of one); endpoints kept in registers, lags per probe.
+  const int per = (m + 31) / 32;
+  const bool regrows = per <= ROOT_ROWS && !devs_serial;
+  int rsd[ROOT_ROWS], rl[ROOT_ROWS];  // rsd: src | dst << 16 (-1: no row)
+#pragma unroll
+  for (int i = 0; i < ROOT_ROWS; ++i) {
+    const int r = lane * per + i;
+    const bool on = regrows && i < per && r < m;
+    rsd[i] = on ? (rsrc[r] | (rdst[r] << 16)) : -1;
+    rl[i] = 0;
+  }
   unsigned long long s_probe = 0, s_root = 0;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + wib; t < n_in; t += nwarps) {
@@ -313,7 +396,54 @@ __global__ void __launch_bounds__(256) k_root(const int *__restrict__ gpool,
       }
       fail = __any_sync(WRX_FULL, bad);
     }
-    for (int round = 0; !fail; ++round) {
+    if (regrows && !fail) {
+#pragma unroll
+      for (int i = 0; i < ROOT_ROWS; ++i) {
+        const int r = lane * per + i;
+        if (rsd[i] >= 0)
+          rl[i] = rbase[r] - (r < ndep ? av[rsd[i] & 0xffff] - av[rsd[i] >> 16] : 1) * P;
+      }
+      for (int round = 0;; ++round) {
+        bool changed = false, bad = false;
+#pragma unroll
+        for (int i = 0; i < ROOT_ROWS; ++i) {
+          if (rsd[i] < 0) continue;
+          const int sr = rsd[i] & 0xffff, ds = rsd[i] >> 16;
+          const int nl = w.lo[sr] + rl[i];
+          if (nl > w.lo[ds]) {
+            atomicMax(&w.lo[ds], nl);
+            changed = true;
+            bad |= nl > w.hi[ds];
+          }
+        }
+#pragma unroll
+        for (int i = ROOT_ROWS - 1; i >= 0; --i) {
+          if (rsd[i] < 0) continue;
+          const int sr = rsd[i] & 0xffff, ds = rsd[i] >> 16;
+          const int nh = w.hi[ds] - rl[i];
+          if (nh < w.hi[sr]) {
+            atomicMin(&w.hi[sr], nh);
+            changed = true;
+            bad |= nh < w.lo[sr];
+          }
+        }
+        __syncwarp();
+        if (__any_sync(WRX_FULL, bad)) {
+          fail = true;
+          break;
+        }
+        if (!__any_sync(WRX_FULL, changed)) {  // fixpoint: any crossing left over?
+          for (int i = lane; i < K; i += 32) bad |= w.lo[i] > w.hi[i];
+          fail = __any_sync(WRX_FULL, bad);
+          break;
+        }
+        if (round >= K) {  // still moving after K+1 rounds: positive cycle
+          fail = true;
+          break;
+        }
+      }
+    }
+    for (int round = 0; !fail && !regrows; ++round) {
       bool changed = false;
       for (int r = lane; r < m; r += 32) {
         const int s = rsrc[r], d = rdst[r];
@@ -336,8 +466,11 @@ __global__ void __launch_bounds__(256) k_root(const int *__restrict__ gpool,
       else if (!__any_sync(WRX_FULL, changed)) break;
       else if (round >= K) fail = true;  // still moving after K+1 rounds: positive cycle
     }
-    if (!fail)
-      for (int d = 0; d < D && !fail; ++d) fail = !wrx_dev_ok(v, w, d);
+    if (!fail) {
+      if (batched) fail = !root_devs_ok(sp, w, ea, ee, ed, nmemb, q0, q1);
+      else
+        for (int d = 0; d < D && !fail; ++d) fail = !wrx_dev_ok(v, w, d);
+    }
     ++s_probe;
     if (lane == 0) {
       if (fail) o.act_out[atomicAdd(&o.counters[0], 1)] = widx;
@@ -1087,6 +1220,13 @@ bool dj_split() {
   return m && std::string(m) == "1";
 }
 
+// TSL_ROOT_DEVS=serial: k_root checks the devices one after another
+// (wrx_dev_ok) instead of all memberships at once (cross-validation)
+bool root_devs_serial() {
+  const char *m = getenv("TSL_ROOT_DEVS");
+  return m && std::string(m) == "serial";
+}
+
 // TSL_RESOLVE_DYN=0 restores the static grid stride of k_resolve_warp
 // (default: probes handed out one at a time through a launch counter)
 bool resolve_dynamic() {
@@ -1640,7 +1780,8 @@ int tsl_engine_probe(tsl_engine *e, int period, int64_t node_budget, int64_t sma
     COUNT_LAUNCH();
     k_root<<<(int)rblocks, 32 * wpb, smem, e->stream>>>(e->d_pool, e->d_assign,
                                                         e->d_act[e->cur], (int)n_in, o,
-                                                        e->d_surv, period, icap, widx_limit);
+                                                        e->d_surv, period, icap, widx_limit,
+                                                        root_devs_serial() ? 1 : 0);
     CK(cudaGetLastError());
     CK(cudaEventRecord(e->evm, e->stream));
     root_timed = true;
