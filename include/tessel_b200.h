@@ -226,7 +226,8 @@ int tsl_validate(int K, int D, const int32_t *dur, const int32_t *mem, const uin
 
 /* Process-wide counters of the subtree-parallel decide: solves, rounds,
  * tasks, replays, nested sub-solves, master nodes, master wall ms, task wall
- * ms (out[8]). */
+ * ms, donated pieces, tasks re-run undivided, nodes explored by task
+ * launches (out[11]). */
 void tsl_sp_stats(double *out);
 
 #ifdef __cplusplus

@@ -50,6 +50,8 @@ __host__ __device__ inline long long sp_task_words(int n) {
   const long long nn = n > 0 ? n : 1;
   return 3 * nn + 2 * sp_nw(n) + 2;
 }
+// donated piece result: status, nodes (2 words), moved, s[n]
+__host__ __device__ inline long long sp_pres_words(int n) { return 4 + (n > 0 ? n : 1); }
 __host__ __device__ inline long long sp_result_words(int n) {
   const long long nn = n > 0 ? n : 1;
   return 4 + sp_nw(n) + nn;
@@ -88,6 +90,20 @@ __device__ inline void sp_load(WWs &w, const int *lo, const int *hi, const int *
   for (int i = lane; i < nw; i += 32) {
     w.placed[i] = placed[i];
     w.inq[i] = inq[i];
+  }
+  __syncwarp();
+}
+// the same from a record another SM wrote during this launch (L2, not L1)
+__device__ inline void sp_load_cg(WWs &w, const int *rec, int n) {
+  const int lane = wrx_lane(), nw = sp_nw(n);
+  for (int i = lane; i < n; i += 32) {
+    w.lo[i] = __ldcg(rec + i);
+    w.hi[i] = __ldcg(rec + n + i);
+    w.s[i] = __ldcg(rec + 2 * n + i);
+  }
+  for (int i = lane; i < nw; i += 32) {
+    w.placed[i] = (unsigned)__ldcg(rec + 3 * n + i);
+    w.inq[i] = (unsigned)__ldcg(rec + 3 * n + nw + i);
   }
   __syncwarp();
 }
@@ -140,13 +156,142 @@ struct SpCut {
   const long long *pre;  // per task: master nodes before it (this walk)
   long long base, budget;
   int k;
+  long long published;   // (donation mode) own nodes already added to part[k]
 };
+
+// Dynamic donation (work splitting inside a task launch).  Idle task warps
+// claim queue slots beyond the launch's tasks; a running piece that sees a
+// claimed-but-unfilled slot gives away "the rest of depth d from value
+// vstack[d] + 1" for the SHALLOWEST depth d >= its floor that still has
+// untried values, and clamps d in its own snapshot so that it never returns
+// there.  In DFS order a piece's own exploration comes first, then its
+// donated pieces, deepest donation first (each later donation is deeper:
+// every depth <= the previous donation's is exhausted for the donor).  A
+// piece runs on the speculation S_in = the task's S (donation only while the
+// donor's sticky set equals it; any piece ending with another set makes the
+// host re-run the task undivided).  Every piece explores its own subtree in
+// DFS order, so a stopped piece still bounds the DFS prefix: the host walks
+// a task's pieces in DFS order (sp_host.inc, sp_combine).
+struct SpDon {
+  unsigned *ctl;           // [0] claims  [1] slots reserved  [2] pieces outstanding
+  int *precs;              // piece records (sp_task_words each)
+  int *pmeta;              // per piece: task, parent slot, depth, ready
+  int *pres;               // per piece: status, nodes (2 words), moved, witness[n]
+  long long *pnodes;       // per slot: own nodes explored so far (published)
+  long long *psub;         // per slot: nodes of its subtree of pieces (published)
+  int *plast;              // per slot: its latest donation (-1: none)
+  int *pprev;              // per piece: its donor's previous donation (-1: none)
+  int count, cap;          // task slots of the launch; piece capacity
+  int self, parent;        // this piece's slot; its donor's slot (-1 for a task)
+  const unsigned *s_in;    // the task's sticky set
+  int every;               // donation check interval (nodes, power of two)
+  int force;               // donate at every check (testing)
+};
+
+// Published nodes that precede this piece in DFS order inside its task:
+// for every donor A on its chain, A's own nodes and the subtree totals of
+// A's donations made after the one this piece descends from (those come
+// first in DFS order).  Lane 0 only.
+__device__ inline long long sp_prefix_nodes(const SpDon &d) {
+  long long s = 0;
+  for (int b = d.self, a = d.parent; a >= 0;) {
+    s += ((volatile long long *)d.pnodes)[a];
+    for (int c = ((volatile int *)d.plast)[a]; c >= 0 && c != b;
+         c = ((volatile int *)d.pprev)[c - d.count])
+      s += ((volatile long long *)d.psub)[c];
+    if (a < d.count) break;
+    b = a;
+    a = ((volatile int *)d.pmeta)[4 * (a - d.count) + 1];
+  }
+  return s;
+}
+
+// Publish `delta` more own nodes of this piece into its subtree total and
+// every donor's.  Lane 0 only.
+__device__ inline void sp_publish_sub(const SpDon &d, long long delta) {
+  if (!delta) return;
+  for (int a = d.self; a >= 0;) {
+    atomicAdd((unsigned long long *)&d.psub[a], (unsigned long long)delta);
+    if (a < d.count) break;
+    a = ((volatile int *)d.pmeta)[4 * (a - d.count) + 1];
+  }
+}
+
+// Give away the rest of the shallowest donatable depth (see SpDon).  Called
+// by the whole warp between nodes: depths < depth hold valid snapshots and
+// vstack entries.
+template <class M>
+__device__ void sp_donate(const M &md, WWs &w, SpDon &d, int floor, int depth, int task) {
+  const int n = md.n(), nw = sp_nw(n), lane = wrx_lane();
+  int want = 0;
+  if (lane == 0) {
+    const unsigned head = ((volatile unsigned *)d.ctl)[0], tail = ((volatile unsigned *)d.ctl)[1];
+    want = (d.force || head > tail) && tail < (unsigned)(d.count + d.cap);
+  }
+  if (!__shfl_sync(WRX_FULL, want, 0)) return;
+  bool diff = false;
+  for (int i = lane; i < nw; i += 32) diff |= w.inq[i] != d.s_in[i];
+  if (__any_sync(WRX_FULL, diff)) return;
+  int dd = -1;
+  for (int b = floor; b < depth && dd < 0; b += 32) {
+    const int j = b + lane;
+    bool ok = false;
+    if (j < depth) ok = w.vstack[j] + 1 <= w.snap[(long long)j * n + md.order(j)].y;
+    const unsigned m = __ballot_sync(WRX_FULL, ok);
+    if (m) dd = b + __ffs(m) - 1;
+  }
+  if (dd < 0) return;
+  int slot = 0;
+  if (lane == 0) slot = (int)atomicAdd(&d.ctl[1], 1u);
+  slot = __shfl_sync(WRX_FULL, slot, 0);
+  const int p = slot - d.count;
+  if (p >= d.cap) return;  // raced past the capacity: keep the work
+  if (lane == 0) atomicAdd(&d.ctl[2], 1u);
+  int *rec = d.precs + (long long)p * sp_task_words(n);
+  const int2 *sn = w.snap + (long long)dd * n;
+  for (int i = lane; i < n; i += 32) {
+    const int2 q = sn[i];
+    rec[i] = q.x;
+    rec[n + i] = q.y;
+    rec[2 * n + i] = w.s[i];
+  }
+  // placed at the piece's entry: the items of depths < dd
+  for (int i = lane; i < nw; i += 32) {
+    unsigned m = 0;
+    for (int j = 0; j < dd; ++j) {
+      const int x = md.order(j);
+      if ((x >> 5) == i) m |= 1u << (x & 31);
+    }
+    rec[3 * n + i] = (int)m;
+    rec[3 * n + nw + i] = (int)w.inq[i];
+  }
+  __syncwarp();  // every lane has read the snapshot before lane 0 clamps it
+  if (lane == 0) {
+    rec[3 * n + 2 * nw] = w.vstack[dd] + 1;
+    rec[3 * n + 2 * nw + 1] = dd;
+    int *pm = d.pmeta + 4 * p;
+    pm[0] = task;
+    pm[1] = d.self;
+    pm[2] = dd;
+    d.pprev[p] = ((volatile int *)d.plast)[d.self];
+    // the donor never returns to depth dd: its snapshot's hi of the item
+    // placed there ends at the value it holds
+    w.snap[(long long)dd * n + md.order(dd)].y = w.vstack[dd];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    ((volatile int *)d.plast)[d.self] = slot;     // first in DFS order among the donations
+    ((volatile int *)d.pmeta)[4 * p + 3] = 1;  // ready
+  }
+  __syncwarp();
+}
 
 template <class M>
 __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth, int &v,
                           long long budget, long long base_nodes, long long *nodes_io,
                           SpSink *sink, long long pause_nodes = 0, int *hist = nullptr,
-                          const SpCut *cut = nullptr) {
+                          SpCut *cut = nullptr, SpDon *don = nullptr, int task = -1) {
   const int n = md.n(), cap = md.cap();
   const int lane = wrx_lane();
   long long nodes = *nodes_io;
@@ -261,12 +406,33 @@ __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth,
       long long sum = 0;
       for (int j = lane; j < cut->k; j += 32) sum += ((volatile long long *)cut->part)[j];
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(WRX_FULL, sum, o);
-      if (lane == 0) ((volatile long long *)cut->part)[cut->k] = nodes;
-      if (cut->base + cut->pre[cut->k] + sum > cut->budget) {
-        status = RX_ABORT;
-        break;
+      if (!don) {
+        if (lane == 0) ((volatile long long *)cut->part)[cut->k] = nodes;
+        if (cut->budget > 0 && cut->base + cut->pre[cut->k] + sum > cut->budget) {
+          status = RX_ABORT;
+          break;
+        }
+      } else {
+        // pieces of one task add up in part[k]; the DFS prefix before this
+        // node also holds every donor's own nodes and this piece's own
+        long long anc = 0;
+        if (lane == 0) {
+          atomicAdd((unsigned long long *)&cut->part[cut->k],
+                    (unsigned long long)(nodes - cut->published));
+          ((volatile long long *)don->pnodes)[don->self] = nodes;
+          sp_publish_sub(*don, nodes - cut->published);
+          anc = sp_prefix_nodes(*don);
+        }
+        anc = __shfl_sync(WRX_FULL, anc, 0);
+        cut->published = nodes;
+        if (cut->budget > 0 && cut->base + cut->pre[cut->k] + sum + anc + nodes > cut->budget) {
+          status = RX_ABORT;
+          break;
+        }
       }
     }
+    if (don && (nodes & (don->every - 1)) == 0 && depth > floor)
+      sp_donate(md, w, *don, floor, depth, task);
     {
       int2 *sn = w.snap + (long long)depth * n;
       for (int i = lane; i < n; i += 32) sn[i] = make_int2(w.lo[i], w.hi[i]);

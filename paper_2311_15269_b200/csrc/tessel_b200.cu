@@ -1110,7 +1110,8 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
                                                   int count, int split, long long budget,
                                                   int *snaps, int *results, int *info,
                                                   long long *part, const long long *pre,
-                                                  long long cut_base, long long cut_budget) {
+                                                  long long cut_base, long long cut_budget,
+                                                  SpDon dq) {
   extern __shared__ int sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const GenView g = gen_view(pool);
@@ -1119,34 +1120,115 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   WWs w = wrx_carve(sm + wib * per_warp, snaps + gw * 2LL * n * (n + 1), n, pool[G_MAXDI]);
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long t = first + gw; t < first + count; t += nwarps) {
-    const int *rec = tasks + t * sp_task_words(n);
-    sp_load(w, rec, rec + n, rec + 2 * n, (const unsigned *)(rec + 3 * n),
-            (const unsigned *)(rec + 3 * n + nw), n);
-    int v = rec[3 * n + 2 * nw], depth = rec[3 * n + 2 * nw + 1];
+  if (!dq.ctl) {  // static: one warp per task
+    for (long long t = first + gw; t < first + count; t += nwarps) {
+      const int *rec = tasks + t * sp_task_words(n);
+      sp_load(w, rec, rec + n, rec + 2 * n, (const unsigned *)(rec + 3 * n),
+              (const unsigned *)(rec + 3 * n + nw), n);
+      int v = rec[3 * n + 2 * nw], depth = rec[3 * n + 2 * nw + 1];
+      long long nodes = 0;
+      SpCut cut{part, pre, cut_base, cut_budget, (int)t, 0};
+      const int st = sp_explore(g, w, depth, n + 1, depth, v, budget, 0, &nodes, nullptr, 0,
+                                nullptr, cut_budget > 0 ? &cut : nullptr);
+      if (lane == 0 && cut_budget > 0) ((volatile long long *)part)[t] = nodes;
+      int *res = results + t * sp_result_words(n);
+      bool moved = false;  // S_out != S_in: the master's speculation failed here
+      for (int i = lane; i < nw; i += 32) moved |= w.inq[i] != (unsigned)rec[3 * n + nw + i];
+      moved = __any_sync(WRX_FULL, moved);
+      if (lane == 0) {
+        res[0] = st;
+        res[1] = (int)(nodes & 0xffffffffLL);
+        res[2] = (int)(nodes >> 32);
+        res[3] = moved ? 1 : 0;
+        info[4 * t + 0] = st;
+        info[4 * t + 1] = res[1];
+        info[4 * t + 2] = res[2];
+        info[4 * t + 3] = res[3];
+      }
+      for (int i = lane; i < nw; i += 32) res[4 + i] = (int)w.inq[i];
+      if (st == RX_SAT)
+        for (int i = lane; i < n; i += 32) res[4 + nw + i] = w.s[i];
+      __syncwarp();
+    }
+    return;
+  }
+  // dynamic: claim slots (tasks first, then donated pieces) until every
+  // piece of the launch is done (SpDon)
+  for (;;) {
+    int slot = 0;
+    if (lane == 0) slot = (int)atomicAdd(&dq.ctl[0], 1u);
+    slot = __shfl_sync(WRX_FULL, slot, 0);
+    const int *rec;
+    long long t;
+    int parent = -1;
+    if (slot < count) {
+      t = first + slot;
+      rec = tasks + t * sp_task_words(n);
+    } else {
+      const int p = slot - count;
+      if (p >= dq.cap) break;
+      int ok = 0;
+      if (lane == 0) {
+        for (;;) {
+          if (((volatile int *)dq.pmeta)[4 * p + 3]) {
+            ok = 1;
+            break;
+          }
+          if (((volatile unsigned *)dq.ctl)[2] == 0u) break;
+          __nanosleep(256);
+        }
+        __threadfence();
+      }
+      ok = __shfl_sync(WRX_FULL, ok, 0);
+      if (!ok) break;
+      rec = dq.precs + (long long)p * sp_task_words(n);
+      t = ((volatile int *)dq.pmeta)[4 * p];
+      parent = ((volatile int *)dq.pmeta)[4 * p + 1];
+    }
+    __syncwarp();
+    sp_load_cg(w, rec, n);
+    int v = __ldcg(rec + 3 * n + 2 * nw), depth = __ldcg(rec + 3 * n + 2 * nw + 1);
     long long nodes = 0;
-    const SpCut cut{part, pre, cut_base, cut_budget, (int)t};
+    SpCut cut{part, pre, cut_base, cut_budget, (int)t, 0};
+    SpDon d = dq;
+    d.self = slot;
+    d.parent = parent;
+    d.s_in = (const unsigned *)(tasks + t * sp_task_words(n) + 3 * n + nw);
     const int st = sp_explore(g, w, depth, n + 1, depth, v, budget, 0, &nodes, nullptr, 0,
-                              nullptr, cut_budget > 0 ? &cut : nullptr);
-    if (lane == 0 && cut_budget > 0) ((volatile long long *)part)[t] = nodes;
-    int *res = results + t * sp_result_words(n);
-    bool moved = false;  // S_out != S_in: the master's speculation failed here
-    for (int i = lane; i < nw; i += 32) moved |= w.inq[i] != (unsigned)rec[3 * n + nw + i];
+                              nullptr, &cut, &d, (int)t);
+    bool moved = false;  // S_out != the task's S_in
+    for (int i = lane; i < nw; i += 32) moved |= w.inq[i] != (unsigned)__ldcg((const int *)d.s_in + i);
     moved = __any_sync(WRX_FULL, moved);
+    if (lane == 0) {
+      atomicAdd((unsigned long long *)&part[t], (unsigned long long)(nodes - cut.published));
+      ((volatile long long *)dq.pnodes)[slot] = nodes;
+      sp_publish_sub(d, nodes - cut.published);
+    }
+    // a task's own result goes to its task slot, a piece's to its piece slot
+    int *res = slot < count ? results + t * sp_result_words(n)
+                            : dq.pres + (long long)(slot - count) * sp_pres_words(n);
+    const int wit_at = slot < count ? 4 + nw : 4;
     if (lane == 0) {
       res[0] = st;
       res[1] = (int)(nodes & 0xffffffffLL);
       res[2] = (int)(nodes >> 32);
       res[3] = moved ? 1 : 0;
-      info[4 * t + 0] = st;
-      info[4 * t + 1] = res[1];
-      info[4 * t + 2] = res[2];
-      info[4 * t + 3] = res[3];
+      if (slot < count) {
+        info[4 * t + 0] = st;
+        info[4 * t + 1] = res[1];
+        info[4 * t + 2] = res[2];
+        info[4 * t + 3] = res[3];
+      }
     }
-    for (int i = lane; i < nw; i += 32) res[4 + i] = (int)w.inq[i];
+    if (slot < count)
+      for (int i = lane; i < nw; i += 32) res[4 + i] = (int)w.inq[i];
     if (st == RX_SAT)
-      for (int i = lane; i < n; i += 32) res[4 + nw + i] = w.s[i];
+      for (int i = lane; i < n; i += 32) res[wit_at + i] = w.s[i];
     __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicSub(&dq.ctl[2], 1u);
+    }
   }
 }
 
@@ -2409,9 +2491,11 @@ float tsl_engine_last_root_ms(tsl_engine *e) { return e ? e->last_root_ms : 0.f;
 
 void tsl_sp_stats(double *out) {
   const SpStats &s = sp_stats();
-  const double v[8] = {(double)s.solves, (double)s.rounds, (double)s.tasks, (double)s.replays,
-                       (double)s.subsolves, (double)s.master_nodes, s.master_ms, s.task_ms};
-  for (int i = 0; i < 8; ++i) out[i] = v[i];
+  const double v[11] = {(double)s.solves,       (double)s.rounds,       (double)s.tasks,
+                        (double)s.replays,      (double)s.subsolves,    (double)s.master_nodes,
+                        s.master_ms,            s.task_ms,              (double)s.pieces,
+                        (double)s.undivided,    (double)s.explored};
+  for (int i = 0; i < 11; ++i) out[i] = v[i];
 }
 
 }  // extern "C"

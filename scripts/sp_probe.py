@@ -13,7 +13,7 @@ from paper_2311_15269_b200 import _native  # noqa: E402
 def main(name, idx):
     d = json.loads(gzip.open(Path(__file__).resolve().parents[1] / "tests" / "golden" /
                              f"probes_{name}.json.gz").read())["probes"]
-    ps = [p for p in d if p["nodes"] >= 1_000_000]
+    ps = [p for p in d if p["nodes"] >= 1_000_000 or (len(sys.argv) > 3 and p["nodes"] > 20_000)]
     p = ps[int(idx)]
     args = (p["n"], p["dur"], p["devmask"], p["mem"], p["edges"], p["order"], p["lo"], p["hi"],
             p["ndev"], p["init"], p["cap"], p["budget"])

@@ -474,3 +474,22 @@ def test_decide_k16_sixteen_microbatches_vs_oracle(gpu):
                             prob["order"], prob["lo"], prob["hi"], prob["ndev"],
                             prob["init_mem"], prob["cap"], budget)
         assert got == (exp[0], exp[1], exp[2]), (horizon, budget, got[0], got[2], exp[0], exp[2])
+
+
+@pytest.mark.parametrize("env", [{"TSL_SP_DONATE": "0"},
+                                 {"TSL_SP_DONATE_FORCE": "1", "TSL_SP_DONATE_EVERY": "16"},
+                                 {"TSL_SP_DONATE_FORCE": "1", "TSL_SP_DONATE_EVERY": "1"},
+                                 {"TSL_SP_DONATE_EVERY": "8", "TSL_SP_PAUSE": "4096"}])
+def test_subtree_parallel_donation_exact(gpu, monkeypatch, env):
+    """Task launches that split their subtrees dynamically (idle warps take
+    the shallowest untried siblings of running pieces; forced donation at
+    every check builds deep piece trees and fills the piece queue) settle
+    every long golden probe exactly: status, lex-min witness, node count."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    probes = [p for name in probe_names() for p in load_probes(name)
+              if (p["budget"] >= 1_000_000 or p["budget"] == 0) and p["nodes"] > 20_000]
+    assert len(probes) >= 10
+    for p in probes:
+        got = gpu.decide_batch([_problem(p)])[0]
+        assert got == (p["status"], p["starts"], p["nodes"]), (p["n"], p["status"], p["nodes"])
