@@ -835,7 +835,8 @@ __global__ void __launch_bounds__(256, 4) k_dj_filter(const int *__restrict__ gp
                                                    ProbeOut o, int *__restrict__ keep, int P,
                                                    long long dj_budget, int cap,
                                                    long long widx_limit, int *gscratch,
-                                                   long long gwords, const int *dev_limit) {
+                                                   long long gwords, const int *dev_limit,
+                                                   int *next) {
   extern __shared__ int sp[];
   load_pool(sp, gpool);
   const int K = sp[R_K];
@@ -848,7 +849,15 @@ __global__ void __launch_bounds__(256, 4) k_dj_filter(const int *__restrict__ gp
   WdjWs w = wdj_carve(mine, gscratch + gw * gwords, K, sp[R_NPAIR]);
   unsigned long long s_dju = 0, s_djn = 0;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long t = gw; t < n_def; t += nwarps) {
+  // probes handed out through a launch counter (heavy-tailed filter costs),
+  // or a static grid stride without one
+  for (long long t = gw;; t += nwarps) {
+    if (next) {
+      int tt = 0;
+      if (lane == 0) tt = atomicAdd(next, 1);
+      t = __shfl_sync(WRX_FULL, tt, 0);
+    }
+    if (t >= n_def) break;
     const int widx = def_in[t];
     if (widx > widx_limit) continue;
     int l = 0;
@@ -1355,9 +1364,10 @@ void run_decide_batch(int count, const tsl_problem *probs, double budget_secs, i
   // (short: the problems it leaves open restart with the subtree-parallel
   // decide's own sample, profiles/r01i_sp_first_sweep.log)
   const long long first = sp ? sp_env("TSL_SP_BATCH_FIRST", 1024) : 0;
+  const long long sp_min = sp_env("TSL_SP_MIN_BUDGET", SP_MIN_BUDGET);
   if (sp)
     for (int i = 0; i < count; ++i)
-      if (budgets[i] == 0 || budgets[i] >= SP_MIN_BUDGET) budgets[i] = first;
+      if (budgets[i] == 0 || budgets[i] >= sp_min) budgets[i] = first;
   if (stride < max_n) throw tsl::Error(TSL_EINVAL, "starts stride smaller than a problem size");
   DecideCtx &ctx = decide_ctx();
   std::lock_guard<std::mutex> lock(ctx.mu);
@@ -1625,6 +1635,14 @@ struct tsl_engine {
 
 // ------------------------------------------------------------------ C ABI
 
+#ifdef WDJ_COUNT_ROUNDS
+extern "C" void tsl_debug_wdj_rounds(unsigned long long *out) {
+  CK(cudaMemcpyFromSymbol(out, g_wdj_rounds, 8));
+  CK(cudaMemcpyFromSymbol(out + 1, g_wdj_calls, 8));
+  CK(cudaMemcpyFromSymbol(out + 2, g_wdj_rows, 8));
+  CK(cudaMemcpyFromSymbol(out + 3, g_wdj_pairs, 8));
+}
+#endif
 extern "C" {
 
 const char *tsl_last_error(void) { return g_err.c_str(); }
@@ -1926,9 +1944,9 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
   const int icap = cap < 0 ? -1 : (int)std::min<int64_t>(cap, tsl::VMAX - 1);
   const long long n_def = e->n_def;
   // continue appending to the level's SAT list and to the active list
-  int counters[6] = {(int)e->n_act, (int)e->n_sat, 0, 0,
-                     (int)std::min<int64_t>(widx_limit, 0x7fffffff), 0};
-  h2d(e->d_counters, counters, 6 * sizeof(int), e->stream);
+  int counters[7] = {(int)e->n_act, (int)e->n_sat, 0, 0,
+                     (int)std::min<int64_t>(widx_limit, 0x7fffffff), 0, 0};
+  h2d(e->d_counters, counters, 7 * sizeof(int), e->stream);
   CK(cudaMemsetAsync(e->d_stats, 0, 8 * sizeof(unsigned long long), e->stream));
   const int threads = 128;
   long long blocks = (n_def + threads - 1) / threads;
@@ -1962,7 +1980,8 @@ int tsl_engine_resolve(tsl_engine *e, int period, int64_t node_budget, int64_t s
     COUNT_LAUNCH();
     k_dj_filter<<<(int)dblocks, 32 * wpb, smem, e->stream>>>(
         e->d_pool, e->d_assign, e->d_def[e->dcur], (int)n_def, o, e->d_surv, period,
-        dj_budget, icap, widx_limit, e->d_ws, gwords, e->d_counters + 4);
+        dj_budget, icap, widx_limit, e->d_ws, gwords, e->d_counters + 4,
+        resolve_dynamic() ? e->d_counters + 6 : nullptr);
     CK(cudaGetLastError());
     rx_in = e->d_surv;
     rx_count = e->d_counters + 3;

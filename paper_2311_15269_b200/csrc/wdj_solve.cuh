@@ -87,10 +87,26 @@ __device__ __forceinline__ bool wdj_bit(const unsigned *b, int q) {
 // touch a changed item (R_ROWCM / R_PAIRCM) — a row or pair none of whose
 // items changed cannot change anything — and collects the items it changed
 // for the next round.
+#ifdef WDJ_COUNT_ROUNDS  // scripts/dj_rounds.py: propagation statistics
+__device__ unsigned long long g_wdj_rounds, g_wdj_calls, g_wdj_rows, g_wdj_pairs;
+#endif
 __device__ inline bool wdj_propagate(const WdjCtx &c, WdjWs &w, unsigned long long cur) {
   const int lane = wrx_lane();
   int quiet = 0;  // rounds since the last new orientation
+#ifdef WDJ_COUNT_ROUNDS
+  if (lane == 0) atomicAdd(&g_wdj_calls, 1ull);
+#endif
   for (;;) {
+#ifdef WDJ_COUNT_ROUNDS
+    if (lane == 0) {
+      atomicAdd(&g_wdj_rounds, 1ull);
+      unsigned long long rc = 0, pc = 0;
+      for (int base = 0; base < c.m; base += 32) rc += (wdj_u64(c.rowcm + 2 * (base >> 5)) & cur) != 0;
+      for (int base = 0; base < c.npair; base += 32) pc += (wdj_u64(c.paircm + 2 * (base >> 5)) & cur) != 0;
+      atomicAdd(&g_wdj_rows, rc);
+      atomicAdd(&g_wdj_pairs, pc);
+    }
+#endif
     bool oriented = false, fail = false;
     unsigned long long mine = 0;
     for (int base = 0; base < c.m; base += 32) {
