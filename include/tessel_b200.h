@@ -227,7 +227,7 @@ int tsl_validate(int K, int D, const int32_t *dur, const int32_t *mem, const uin
 /* Process-wide counters of the subtree-parallel decide: solves, rounds,
  * tasks, replays, nested sub-solves, master nodes, master wall ms, task wall
  * ms, donated pieces, tasks re-run undivided, nodes explored by task
- * launches (out[11]). */
+ * launches, sticky-set epochs (out[12]). */
 void tsl_sp_stats(double *out);
 
 #ifdef __cplusplus

@@ -174,10 +174,10 @@ def counters() -> dict:
 
 def sp_stats() -> dict:
     """Counters of the subtree-parallel decide (csrc/sp_host.inc)."""
-    a = np.zeros(11, dtype=np.float64)
+    a = np.zeros(12, dtype=np.float64)
     lib().tsl_sp_stats(_ptr(a))
     keys = ("solves", "rounds", "tasks", "replays", "subsolves", "master_nodes", "master_ms",
-            "task_ms", "pieces", "undivided", "explored")
+            "task_ms", "pieces", "undivided", "explored", "epochs")
     return {k: float(v) for k, v in zip(keys, a)}
 
 

@@ -34,6 +34,7 @@
 
 #define SP_EXHAUSTED 4  // subtree / sub-range exhausted (backtracked below the floor)
 #define SP_PAUSED 5     // master stopped after emitting its task quota
+#define SP_INVALID 8    // piece stopped: a piece before it in DFS order ended with another sticky set
 
 __host__ __device__ inline int sp_nw(int n) { return ((n > 0 ? n : 1) + 31) / 32; }
 // words before the snapshot area, rounded up so the int2 snapshots are aligned
@@ -50,8 +51,10 @@ __host__ __device__ inline long long sp_task_words(int n) {
   const long long nn = n > 0 ? n : 1;
   return 3 * nn + 2 * sp_nw(n) + 2;
 }
-// donated piece result: status, nodes (2 words), moved, s[n]
-__host__ __device__ inline long long sp_pres_words(int n) { return 4 + (n > 0 ? n : 1); }
+// donated piece result: status, nodes (2 words), moved, s[n], inq_out[nw]
+__host__ __device__ inline long long sp_pres_words(int n) {
+  return 4 + (n > 0 ? n : 1) + sp_nw(n);
+}
 __host__ __device__ inline long long sp_result_words(int n) {
   const long long nn = n > 0 ? n : 1;
   return 4 + sp_nw(n) + nn;
@@ -181,6 +184,9 @@ struct SpDon {
   long long *psub;         // per slot: nodes of its subtree of pieces (published)
   int *plast;              // per slot: its latest donation (-1: none)
   int *pprev;              // per piece: its donor's previous donation (-1: none)
+  int *pmoved;             // per slot: 1 = ends the usable DFS prefix (sticky set changed,
+                           // SAT or cap), 2 = a piece in its subtree does
+  int first;               // task index of slot 0
   int count, cap;          // task slots of the launch; piece capacity
   int self, parent;        // this piece's slot; its donor's slot (-1 for a task)
   const unsigned *s_in;    // the task's sticky set
@@ -192,18 +198,34 @@ struct SpDon {
 // for every donor A on its chain, A's own nodes and the subtree totals of
 // A's donations made after the one this piece descends from (those come
 // first in DFS order).  Lane 0 only.
-__device__ inline long long sp_prefix_nodes(const SpDon &d) {
+// *invalid: a piece before it in DFS order (a donor's own part, or a
+// preceding donation's subtree) ended with another sticky set.
+__device__ inline long long sp_prefix_nodes(const SpDon &d, bool *invalid) {
   long long s = 0;
   for (int b = d.self, a = d.parent; a >= 0;) {
     s += ((volatile long long *)d.pnodes)[a];
+    if (((volatile int *)d.pmoved)[a] & 1) *invalid = true;
     for (int c = ((volatile int *)d.plast)[a]; c >= 0 && c != b;
-         c = ((volatile int *)d.pprev)[c - d.count])
+         c = ((volatile int *)d.pprev)[c - d.count]) {
       s += ((volatile long long *)d.psub)[c];
+      if (((volatile int *)d.pmoved)[c] & 2) *invalid = true;
+    }
     if (a < d.count) break;
     b = a;
     a = ((volatile int *)d.pmeta)[4 * (a - d.count) + 1];
   }
   return s;
+}
+
+// A piece ended with another sticky set: flag it and every donor's subtree.
+// Lane 0 only.
+__device__ inline void sp_mark_moved(const SpDon &d) {
+  atomicOr(&d.pmoved[d.self], 3);
+  for (int a = d.parent; a >= 0;) {
+    atomicOr(&d.pmoved[a], 2);
+    if (a < d.count) break;
+    a = ((volatile int *)d.pmeta)[4 * (a - d.count) + 1];
+  }
 }
 
 // Publish `delta` more own nodes of this piece into its subtree total and
@@ -416,15 +438,22 @@ __device__ int sp_explore(const M &md, WWs &w, int floor, int split, int &depth,
         // pieces of one task add up in part[k]; the DFS prefix before this
         // node also holds every donor's own nodes and this piece's own
         long long anc = 0;
+        bool inval = false;
         if (lane == 0) {
           atomicAdd((unsigned long long *)&cut->part[cut->k],
                     (unsigned long long)(nodes - cut->published));
           ((volatile long long *)don->pnodes)[don->self] = nodes;
           sp_publish_sub(*don, nodes - cut->published);
-          anc = sp_prefix_nodes(*don);
+          anc = sp_prefix_nodes(*don, &inval);
         }
+        for (int j = don->first + lane; j < cut->k; j += 32)
+          inval |= (((volatile int *)don->pmoved)[j - don->first] & 2) != 0;
         anc = __shfl_sync(WRX_FULL, anc, 0);
         cut->published = nodes;
+        if (__any_sync(WRX_FULL, inval)) {
+          status = SP_INVALID;
+          break;
+        }
         if (cut->budget > 0 && cut->base + cut->pre[cut->k] + sum + anc + nodes > cut->budget) {
           status = RX_ABORT;
           break;

@@ -1212,6 +1212,10 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
       atomicAdd((unsigned long long *)&part[t], (unsigned long long)(nodes - cut.published));
       ((volatile long long *)dq.pnodes)[slot] = nodes;
       sp_publish_sub(d, nodes - cut.published);
+      // the DFS prefix the host can use ends at this piece: every piece after
+      // it stops (SP_INVALID) — its sticky set changed (an epoch follows),
+      // or the probe is settled here (SAT, cap passed)
+      if (moved || st == RX_SAT || st == RX_ABORT) sp_mark_moved(d);
     }
     // a task's own result goes to its task slot, a piece's to its piece slot
     int *res = slot < count ? results + t * sp_result_words(n)
@@ -1231,12 +1235,30 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
     }
     if (slot < count)
       for (int i = lane; i < nw; i += 32) res[4 + i] = (int)w.inq[i];
+    else
+      for (int i = lane; i < nw; i += 32) res[4 + n + i] = (int)w.inq[i];
     if (st == RX_SAT)
       for (int i = lane; i < n; i += 32) res[wit_at + i] = w.s[i];
     __syncwarp();
     if (lane == 0) {
       __threadfence();
       atomicSub(&dq.ctl[2], 1u);
+    }
+  }
+}
+
+// Copy task records (scattered over the task and piece arrays) into a
+// contiguous task array, with the sticky set replaced by S (sp_host.inc,
+// SpRun::epochs).
+__global__ void k_sp_gather(const unsigned long long *__restrict__ src, int count, int n,
+                            const unsigned *__restrict__ S, int *dst) {
+  const int tw = (int)sp_task_words(n), nw = sp_nw(n);
+  for (int r = blockIdx.x; r < count; r += gridDim.x) {
+    const int *a = (const int *)src[r];
+    int *b = dst + (long long)r * tw;
+    for (int i = threadIdx.x; i < tw; i += blockDim.x) {
+      const int k = i - 3 * n - nw;  // the inq words
+      b[i] = (k >= 0 && k < nw) ? (int)S[k] : a[i];
     }
   }
 }
@@ -2510,11 +2532,11 @@ float tsl_engine_last_root_ms(tsl_engine *e) { return e ? e->last_root_ms : 0.f;
 
 void tsl_sp_stats(double *out) {
   const SpStats &s = sp_stats();
-  const double v[11] = {(double)s.solves,       (double)s.rounds,       (double)s.tasks,
+  const double v[12] = {(double)s.solves,       (double)s.rounds,       (double)s.tasks,
                         (double)s.replays,      (double)s.subsolves,    (double)s.master_nodes,
                         s.master_ms,            s.task_ms,              (double)s.pieces,
-                        (double)s.undivided,    (double)s.explored};
-  for (int i = 0; i < 11; ++i) out[i] = v[i];
+                        (double)s.undivided,    (double)s.explored,     (double)s.epochs};
+  for (int i = 0; i < 12; ++i) out[i] = v[i];
 }
 
 }  // extern "C"

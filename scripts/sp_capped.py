@@ -34,7 +34,7 @@ def main(name, mx=6):
             row[mode] = {"exact": (st, nodes) == (p["status"], p["nodes"]) and
                          (st != 1 or list(starts) == p["starts"]), "wall_s": round(wall, 4),
                          "undivided": s1["undivided"] - s0["undivided"],
-                         "pieces": s1["pieces"] - s0["pieces"], "explored": s1["explored"] - s0["explored"]}
+                         "pieces": s1["pieces"] - s0["pieces"], "explored": s1["explored"] - s0["explored"], "epochs": s1["epochs"] - s0["epochs"]}
         print(json.dumps(row))
 
 

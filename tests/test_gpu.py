@@ -493,3 +493,19 @@ def test_subtree_parallel_donation_exact(gpu, monkeypatch, env):
     for p in probes:
         got = gpu.decide_batch([_problem(p)])[0]
         assert got == (p["status"], p["starts"], p["nodes"]), (p["n"], p["status"], p["nodes"])
+
+
+@pytest.mark.parametrize("env", [{}, {"TSL_SP_DONATE_FORCE": "1", "TSL_SP_DONATE_EVERY": "16"}])
+def test_subtree_parallel_sticky_set_epochs_exact(gpu, monkeypatch, env):
+    """400k-capped repetend probes whose sticky sets change many times, run
+    subtree-parallel: after each change the rest of the task is re-run on
+    the new set (epochs) — status, witness and node count stay exact."""
+    monkeypatch.setenv("TSL_SP_MIN_BUDGET", "1")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    probes = [p for name in ("C3_9", "C4a_3", "nn4_k3") for p in load_probes(name)
+              if p["kind"] == "capped" and p["nodes"] > 50_000][:10]
+    assert len(probes) >= 6
+    for p in probes:
+        got = gpu.decide_batch([_problem(p)])[0]
+        assert got == (p["status"], p["starts"], p["nodes"]), (p["n"], p["status"], p["nodes"])
