@@ -192,6 +192,7 @@ struct SpDon {
   const unsigned *s_in;    // the task's sticky set
   int every;               // donation check interval (nodes, power of two)
   int force;               // donate at every check (testing)
+  int any_s;               // donate on any sticky set (the piece starts on the donor's)
 };
 
 // Published nodes that precede this piece in DFS order inside its task:
@@ -251,9 +252,11 @@ __device__ void sp_donate(const M &md, WWs &w, SpDon &d, int floor, int depth, i
     want = (d.force || head > tail) && tail < (unsigned)(d.count + d.cap);
   }
   if (!__shfl_sync(WRX_FULL, want, 0)) return;
-  bool diff = false;
-  for (int i = lane; i < nw; i += 32) diff |= w.inq[i] != d.s_in[i];
-  if (__any_sync(WRX_FULL, diff)) return;
+  if (!d.any_s) {  // donate only on the piece's own set
+    bool diff = false;
+    for (int i = lane; i < nw; i += 32) diff |= w.inq[i] != d.s_in[i];
+    if (__any_sync(WRX_FULL, diff)) return;
+  }
   int dd = -1;
   for (int b = floor; b < depth && dd < 0; b += 32) {
     const int j = b + lane;

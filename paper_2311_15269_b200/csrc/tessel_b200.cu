@@ -1202,11 +1202,20 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
     SpDon d = dq;
     d.self = slot;
     d.parent = parent;
-    d.s_in = (const unsigned *)(tasks + t * sp_task_words(n) + 3 * n + nw);
+    d.s_in = (const unsigned *)(rec + 3 * n + nw);  // this piece's own speculated set
     const int st = sp_explore(g, w, depth, n + 1, depth, v, budget, 0, &nodes, nullptr, 0,
                               nullptr, &cut, &d, (int)t);
-    bool moved = false;  // S_out != the task's S_in
-    for (int i = lane; i < nw; i += 32) moved |= w.inq[i] != (unsigned)__ldcg((const int *)d.s_in + i);
+    // the set the next piece in DFS order was started on: the latest
+    // donation's (donations come right after the donor's own nodes), else
+    // the one after this piece, speculated equal to this piece's S_in
+    int lastd = -1;
+    if (lane == 0) lastd = ((volatile int *)dq.plast)[slot];
+    lastd = __shfl_sync(WRX_FULL, lastd, 0);
+    const int *snext = lastd >= 0 ? dq.precs + (long long)(lastd - count) * sp_task_words(n) +
+                                        3 * n + nw
+                                  : (const int *)d.s_in;
+    bool moved = false;  // S_out != that set: the DFS prefix the host can use ends here
+    for (int i = lane; i < nw; i += 32) moved |= w.inq[i] != (unsigned)__ldcg(snext + i);
     moved = __any_sync(WRX_FULL, moved);
     if (lane == 0) {
       atomicAdd((unsigned long long *)&part[t], (unsigned long long)(nodes - cut.published));

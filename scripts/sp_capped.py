@@ -20,11 +20,14 @@ def main(name, mx=6):
         args = (p["n"], p["dur"], p["devmask"], p["mem"], p["edges"], p["order"], p["lo"], p["hi"],
                 p["ndev"], p["init"], p["cap"], p["budget"])
         row = {"probe": f"{name}[{i}]", "n": p["n"], "status": p["status"], "nodes": p["nodes"]}
-        for mode in ("warp", "sp"):
-            if mode == "sp":
+        for mode in ("warp", "sp", "sp_any"):
+            os.environ.pop("TSL_SP_DONATE_ANY_S", None)
+            if mode.startswith("sp"):
                 os.environ["TSL_SP_MIN_BUDGET"] = "1"
             else:
                 os.environ.pop("TSL_SP_MIN_BUDGET", None)
+            if mode == "sp_any":
+                os.environ["TSL_SP_DONATE_ANY_S"] = "1"
             _native.decide(*args)
             s0 = _native.sp_stats()
             t0 = time.perf_counter()

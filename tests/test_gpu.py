@@ -495,7 +495,10 @@ def test_subtree_parallel_donation_exact(gpu, monkeypatch, env):
         assert got == (p["status"], p["starts"], p["nodes"]), (p["n"], p["status"], p["nodes"])
 
 
-@pytest.mark.parametrize("env", [{}, {"TSL_SP_DONATE_FORCE": "1", "TSL_SP_DONATE_EVERY": "16"}])
+@pytest.mark.parametrize("env", [{}, {"TSL_SP_DONATE_FORCE": "1", "TSL_SP_DONATE_EVERY": "16"},
+                                 {"TSL_SP_DONATE_ANY_S": "1"},
+                                 {"TSL_SP_DONATE_ANY_S": "1", "TSL_SP_DONATE_FORCE": "1",
+                                  "TSL_SP_DONATE_EVERY": "16"}])
 def test_subtree_parallel_sticky_set_epochs_exact(gpu, monkeypatch, env):
     """400k-capped repetend probes whose sticky sets change many times, run
     subtree-parallel: after each change the rest of the task is re-run on
