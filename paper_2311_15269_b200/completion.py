@@ -12,6 +12,7 @@ and the lazy feasibility checks) runs its decide probes on the GPU too.
 from __future__ import annotations
 
 import bisect
+import gc
 import os
 
 import numpy as np
@@ -375,6 +376,21 @@ def search(p: PlacementSpec, mem_capacity: Optional[int] = None, max_nr: Optiona
     disjunctive refutation settle most probes without the reference's DFS,
     so its node total is not reproduced).  ``report.engine`` holds this
     search's GPU counters."""
+    # the cyclic garbage collector stays off during the search: the scan
+    # allocates many short-lived host objects per level and a full
+    # collection over the caller's heap stalled single searches by
+    # 0.2-0.6 s (profiles/r02i_e2e_var.log); reference counting frees them
+    paused = gc.isenabled()
+    if paused:
+        gc.disable()
+    try:
+        return _search(p, mem_capacity, max_nr, lazy, budget, jobs, device, engine, comm)
+    finally:
+        if paused:
+            gc.enable()
+
+
+def _search(p, mem_capacity, max_nr, lazy, budget, jobs, device, engine, comm):
     cap = mem_capacity
     lb = lower_bound(p)
     total = sum(b.time_cost for b in p.blocks)

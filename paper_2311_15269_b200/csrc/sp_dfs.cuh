@@ -193,7 +193,23 @@ struct SpDon {
   int every;               // donation check interval (nodes, power of two)
   int force;               // donate at every check (testing)
   int any_s;               // donate on any sticky set (the piece starts on the donor's)
+  int *tmade, *tdone;      // per task slot: pieces donated / pieces finished (+1: the task)
+  int slot_task;           // this piece's task slot
+  int window;              // donate only within this many tasks of the leftmost open one (-1: any)
 };
+
+// A piece of task slot ts finished: when it was the task's last one, move the
+// leftmost-open-task mark (ctl[3]) past every finished task.  Lane 0 only.
+__device__ inline void sp_task_piece_done(const SpDon &d, int ts) {
+  __threadfence();
+  atomicAdd(&d.tdone[ts], 1);
+  for (;;) {
+    const unsigned lo = ((volatile unsigned *)d.ctl)[3];
+    if (lo >= (unsigned)d.count) break;
+    if (((volatile int *)d.tdone)[lo] != ((volatile int *)d.tmade)[lo] + 1) break;
+    atomicCAS(&d.ctl[3], lo, lo + 1);
+  }
+}
 
 // Published nodes that precede this piece in DFS order inside its task:
 // for every donor A on its chain, A's own nodes and the subtree totals of
@@ -250,6 +266,10 @@ __device__ void sp_donate(const M &md, WWs &w, SpDon &d, int floor, int depth, i
   if (lane == 0) {
     const unsigned head = ((volatile unsigned *)d.ctl)[0], tail = ((volatile unsigned *)d.ctl)[1];
     want = (d.force || head > tail) && tail < (unsigned)(d.count + d.cap);
+    // help only the leftmost unfinished tasks (DFS order): pieces of later
+    // tasks mostly explore beyond the cap position
+    if (want && d.window >= 0 && !d.force)
+      want = d.slot_task - (int)((volatile unsigned *)d.ctl)[3] <= d.window;
   }
   if (!__shfl_sync(WRX_FULL, want, 0)) return;
   if (!d.any_s) {  // donate only on the piece's own set
@@ -271,7 +291,10 @@ __device__ void sp_donate(const M &md, WWs &w, SpDon &d, int floor, int depth, i
   slot = __shfl_sync(WRX_FULL, slot, 0);
   const int p = slot - d.count;
   if (p >= d.cap) return;  // raced past the capacity: keep the work
-  if (lane == 0) atomicAdd(&d.ctl[2], 1u);
+  if (lane == 0) {
+    atomicAdd(&d.ctl[2], 1u);
+    atomicAdd(&d.tmade[d.slot_task], 1);  // before the piece can finish
+  }
   int *rec = d.precs + (long long)p * sp_task_words(n);
   const int2 *sn = w.snap + (long long)dd * n;
   for (int i = lane; i < n; i += 32) {

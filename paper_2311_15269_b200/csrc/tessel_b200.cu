@@ -1202,6 +1202,7 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
     SpDon d = dq;
     d.self = slot;
     d.parent = parent;
+    d.slot_task = (int)(t - first);
     d.s_in = (const unsigned *)(rec + 3 * n + nw);  // this piece's own speculated set
     const int st = sp_explore(g, w, depth, n + 1, depth, v, budget, 0, &nodes, nullptr, 0,
                               nullptr, &cut, &d, (int)t);
@@ -1250,6 +1251,7 @@ __global__ void __launch_bounds__(128) k_sp_tasks(const int *__restrict__ pool,
       for (int i = lane; i < n; i += 32) res[wit_at + i] = w.s[i];
     __syncwarp();
     if (lane == 0) {
+      sp_task_piece_done(dq, (int)(t - first));
       __threadfence();
       atomicSub(&dq.ctl[2], 1u);
     }
