@@ -479,7 +479,8 @@ def test_decide_k16_sixteen_microbatches_vs_oracle(gpu):
 @pytest.mark.parametrize("env", [{"TSL_SP_DONATE": "0"},
                                  {"TSL_SP_DONATE_FORCE": "1", "TSL_SP_DONATE_EVERY": "16"},
                                  {"TSL_SP_DONATE_FORCE": "1", "TSL_SP_DONATE_EVERY": "1"},
-                                 {"TSL_SP_DONATE_EVERY": "8", "TSL_SP_PAUSE": "4096"}])
+                                 {"TSL_SP_DONATE_EVERY": "8", "TSL_SP_PAUSE": "4096"},
+                                 {"TSL_SP_DONATE_WINDOW": "-1"}, {"TSL_SP_DONATE_WINDOW": "0"}])
 def test_subtree_parallel_donation_exact(gpu, monkeypatch, env):
     """Task launches that split their subtrees dynamically (idle warps take
     the shallowest untried siblings of running pieces; forced donation at
