@@ -73,14 +73,43 @@ class ClockSampler:
         self.rows, self._stop = [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _nvml(self):
+        """In-process NVML sampler (same fields as the nvidia-smi query): a
+        fresh nvidia-smi process every period initialises NVML each time and
+        measurably stalled the e2e leg's CUDA allocation calls."""
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+
+            def sample():
+                r = get(h)
+                return [str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(mx)] + \
+                    ["Active" if r & b else "Not Active" for b in bits]
+            sample()
+            return sample
+        except Exception:
+            return None
+
     def _run(self):
+        sample = self._nvml()
+        self.source = "nvml (in-process)" if sample is not None else "nvidia-smi"
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if sample is not None:
+                    self.rows.append(sample())
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
             self._stop.wait(self.period)
@@ -103,7 +132,7 @@ class ClockSampler:
                           if len(r) > 2 + i and r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "sampler": getattr(self, "source", None)}
 
 
 def _flush_l2(torch, dev):
@@ -390,7 +419,9 @@ def run_b200_arm(args):
                 "h2d_bytes_per_step": (c2["h2d_bytes"] - c1["h2d_bytes"]) // args.steps,
                 "d2h_bytes_per_step": (c2["d2h_bytes"] - c1["d2h_bytes"]) // args.steps,
                 "basis": "search(PlacementSpec) -> Schedule through the public API, fresh "
-                         "engine per step"},
+                         "engine per step",
+                "step_walls_s": [round(x, 4) for x in e2e_walls]},
+        "step_walls_s": [round(x, 4) for x in walls],
         "gpu_launches": launches,
         "work_per_step": per_step,
         "rates": {"candidates_per_s": cands / wall,
