@@ -519,20 +519,22 @@ def _search(p, mem_capacity, max_nr, lazy, budget, jobs, device, engine, comm):
         # this rank's share: reference decides of every candidate that
         # passes the memory gate, at the bound in force at its index
         lo_w, hi_w = a0 - r0, min(a0 - r0 + win.count, used)
-        passing = (np.ones(max(0, hi_w - lo_w), dtype=np.int64) if win.gate is None
-                   else win.gate[:max(0, hi_w - lo_w)].astype(np.int64))
-        cum = np.concatenate(([0], np.cumsum(passing)))
+        gate = win.gate  # 0/1 per candidate of this shard; None: no memory gate
 
         def n_pass(i0, i1):  # window-relative [i0, i1) within this shard
             i0, i1 = max(i0, lo_w), min(i1, hi_w)
-            return int(cum[i1 - lo_w] - cum[i0 - lo_w]) if i1 > i0 else 0
+            if i1 <= i0:
+                return 0
+            if gate is None:
+                return i1 - i0
+            return int(np.count_nonzero(gate[i0 - lo_w:i1 - lo_w]))
 
         opt, prev = opt0, 0
         for widx, new_opt in points:
             acct["decides"] += n_pass(prev, widx + 1) * span(opt)
             opt, prev = new_opt, widx + 1
         acct["decides"] += n_pass(prev, used) * span(opt)
-        acct["infeasible"].append(int(len(passing) - cum[-1]))
+        acct["infeasible"].append(max(0, hi_w - lo_w) - n_pass(lo_w, hi_w))
         log.add_segment(n_r, r0, used, special, None)
         if timed_out and not stop:
             report.timed_out = True
