@@ -34,6 +34,7 @@ unmodified reference package built here; else the oracle port) on the host.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -68,8 +69,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0, period=0.2):
-        self.index, self.period = index, period
+    def __init__(self, index=0, period=None):
+        self.index = index
+        self.period = float(os.environ.get("BENCH_CLOCK_PERIOD", "0.2")) if period is None else period
         self.rows, self._stop = [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
@@ -97,6 +99,9 @@ class ClockSampler:
             return None
 
     def _run(self):
+        if self.period <= 0:  # diagnosis only: no sampling
+            self.source = "off"
+            return
         sample = self._nvml()
         self.source = "nvml (in-process)" if sample is not None else "nvidia-smi"
         while not self._stop.is_set():
@@ -341,6 +346,11 @@ def run_b200_arm(args):
         ok = _matches(res, golden)
         parity = ok if parity is None else (parity and ok)
 
+    # the cyclic GC stays off over both timed legs (search() pauses it
+    # itself; between steps a full collection over the results still held
+    # added 0.3-0.7 s to single e2e steps, profiles/r02l_bench_line.json)
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clk:
         # (1) value: the whole search step with the engine resident (its
         # placement tables and frontier count tables already in HBM)
@@ -385,6 +395,7 @@ def run_b200_arm(args):
         c2 = _native.counters()
         if dist:
             dist.barrier()
+    gc.enable()
     launches = c1["launches"] - c0["launches"]
     wall, e2e_wall = sum(walls), sum(e2e_walls)
     if dist:

@@ -105,7 +105,10 @@ struct DevFree {
 // run: cudaFree synchronises the whole device, which would serialise the
 // asynchronous verification slots behind every buffer growth; the pool's
 // release threshold keeps freed memory cached.
-static void dev_grow(void **p, size_t bytes, cudaStream_t s) {
+// The current device's stream-ordered pool keeps freed memory cached
+// (release threshold: never), so buffers are reused across growths and
+// across engines.
+static void pool_keep() {
   static std::once_flag once;
   std::call_once(once, [] {
     int dev = 0;
@@ -115,6 +118,10 @@ static void dev_grow(void **p, size_t bytes, cudaStream_t s) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   });
+}
+
+static void dev_grow(void **p, size_t bytes, cudaStream_t s) {
+  pool_keep();
   if (*p) CK(cudaFreeAsync(*p, s));
   *p = nullptr;
   CK(cudaMallocAsync(p, bytes, s));
@@ -829,7 +836,10 @@ __host__ __device__ inline int dj_warp_words(const int *pool) {
   return (wdj_smem_words(pool[R_K], pool[R_NPAIR]) + ndep1 + pool[R_D] + 3) & ~3;
 }
 
-__global__ void __launch_bounds__(256, 4) k_dj_filter(const int *__restrict__ gpool,
+#ifndef DJ_FILTER_MINB
+#define DJ_FILTER_MINB 4
+#endif
+__global__ void __launch_bounds__(256, DJ_FILTER_MINB) k_dj_filter(const int *__restrict__ gpool,
                                                    const unsigned char *__restrict__ assign,
                                                    const int *__restrict__ def_in, int n_def,
                                                    ProbeOut o, int *__restrict__ keep, int P,
@@ -1587,11 +1597,15 @@ struct tsl_engine {
       CK(cudaEventCreate(&vs.ev1));
     }
     CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
-    CK(cudaMalloc(&d_pool, pool.size() * sizeof(int)));
+    // every engine buffer comes from the device's stream-ordered pool
+    // (dev_grow keeps its freed memory cached): a fresh engine reuses the
+    // previous one's memory, and its teardown never synchronises the device
+    pool_keep();
+    CK(cudaMallocAsync((void **)&d_pool, pool.size() * sizeof(int), stream));
     h2d(d_pool, pool.data(), pool.size() * sizeof(int), stream);
     CK(cudaStreamSynchronize(stream));
-    CK(cudaMalloc(&d_counters, 8 * sizeof(int)));  // [4] = speculative retirement limit
-    CK(cudaMalloc(&d_stats, 8 * sizeof(unsigned long long)));
+    CK(cudaMallocAsync((void **)&d_counters, 8 * sizeof(int), stream));  // [4] = speculative retirement limit
+    CK(cudaMallocAsync((void **)&d_stats, 8 * sizeof(unsigned long long), stream));
     smem_bytes = pool.size() * sizeof(int);
     if (smem_bytes > 48 * 1024) {
       CK(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1607,7 +1621,8 @@ struct tsl_engine {
     (void)ndep;
     ws_words = rep_ws_words(pool.data());
     ws_threads = num_sms * 4 * 128;
-    CK(cudaMalloc(&d_ws, (size_t)ws_threads * ws_words * sizeof(int)));
+    CK(cudaMallocAsync((void **)&d_ws, (size_t)ws_threads * ws_words * sizeof(int), stream));
+    CK(cudaStreamSynchronize(stream));
     gpu_ready = true;
   }
 
@@ -1645,18 +1660,24 @@ struct tsl_engine {
 
   ~tsl_engine() {
     if (!gpu_ready) return;
+    // stream-ordered frees back into the pool, after the work queued on the
+    // engine's streams (a synchronous cudaFree stalled a caller's next
+    // search by up to 0.5 s); stream and event destruction do not block
+    for (auto &vs : vslot) {
+      cudaStreamWaitEvent(stream, vs.ev1, 0);
+      if (vs.rows) cudaFreeAsync(vs.rows, vs.st);
+      if (vs.buf) cudaFreeAsync(vs.buf, vs.st);
+    }
     for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
                     (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather,
                     (void *)d_def[0], (void *)d_def[1], (void *)d_verify, (void *)d_surv,
                     (void *)d_sat_key, (void *)d_sat_next, (void *)d_stash_idx})
-      if (p) cudaFree(p);
+      if (p) cudaFreeAsync(p, stream);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     cudaEventDestroy(evm);
     for (auto &vs : vslot) {
-      if (vs.rows) cudaFree(vs.rows);
-      if (vs.buf) cudaFree(vs.buf);
       cudaEventDestroy(vs.ev_go);
       cudaEventDestroy(vs.ev0);
       cudaEventDestroy(vs.ev1);
@@ -2317,8 +2338,8 @@ int tsl_engine_sat_next(tsl_engine *e, int64_t after, int64_t *widx_out, int32_t
   *widx_out = -1;
   if (e->n_sat <= 0) return TSL_OK;
   if (!e->d_sat_key) {
-    CK(cudaMalloc(&e->d_sat_key, sizeof(unsigned long long)));
-    CK(cudaMalloc(&e->d_sat_next, (size_t)(K + 1) * sizeof(int)));
+    CK(cudaMallocAsync((void **)&e->d_sat_key, sizeof(unsigned long long), e->stream));
+    CK(cudaMallocAsync((void **)&e->d_sat_next, (size_t)(K + 1) * sizeof(int), e->stream));
   }
   CK(cudaMemsetAsync(e->d_sat_key, 0xff, sizeof(unsigned long long), e->stream));
   const long long n = e->n_sat;
