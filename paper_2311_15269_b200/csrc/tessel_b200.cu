@@ -27,6 +27,8 @@
 #include <thread>
 #include <numeric>
 #include <string>
+#include <map>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/tessel_b200.h"
@@ -120,11 +122,77 @@ static void pool_keep() {
   });
 }
 
+// Idle engine buffers, kept per device for the next engine: a dropped
+// engine's buffers (its streams synchronised first) go here instead of back
+// to the pool, whose cross-stream reuse of freed memory is opportunistic —
+// a fresh engine then mapped ~1 GB of new memory every few searches
+// (0.3-0.8 s stalls, profiles/r02m_e2e_outliers_*.log).
+struct IdleBlocks {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void *> idle;  // (device, bytes) -> block
+  std::unordered_map<void *, size_t> size;             // every pool block we made
+  size_t held = 0;
+};
+static IdleBlocks &idle_blocks() {
+  static IdleBlocks b;
+  return b;
+}
+static constexpr size_t IDLE_MAX = 16ull << 30;  // bytes kept idle per process
+
+// A block of >= bytes: an idle one (at most 2x larger) or a new pool block.
+static void *dev_take(size_t bytes, cudaStream_t s) {
+  pool_keep();
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  IdleBlocks &b = idle_blocks();
+  {
+    std::lock_guard<std::mutex> g(b.mu);
+    auto it = b.idle.lower_bound({dev, bytes});
+    if (it != b.idle.end() && it->first.first == dev && it->first.second <= 2 * bytes + (1 << 20)) {
+      void *p = it->second;
+      b.held -= it->first.second;
+      b.idle.erase(it);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  CK(cudaMallocAsync(&p, bytes, s));
+  std::lock_guard<std::mutex> g(b.mu);
+  b.size[p] = bytes;
+  return p;
+}
+
+// Park an idle block (its users' streams are done with it) for a later
+// engine, or free it when the idle set is full / it is not ours.
+static void dev_park(void *p, cudaStream_t s) {
+  if (!p) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  IdleBlocks &b = idle_blocks();
+  {
+    std::lock_guard<std::mutex> g(b.mu);
+    auto it = b.size.find(p);
+    if (it != b.size.end() && b.held + it->second <= IDLE_MAX) {
+      b.idle.insert({{dev, it->second}, p});
+      b.held += it->second;
+      return;
+    }
+    if (it != b.size.end()) b.size.erase(it);
+  }
+  cudaFreeAsync(p, s);
+}
+
 static void dev_grow(void **p, size_t bytes, cudaStream_t s) {
   pool_keep();
-  if (*p) CK(cudaFreeAsync(*p, s));
-  *p = nullptr;
-  CK(cudaMallocAsync(p, bytes, s));
+  if (*p) {
+    {
+      IdleBlocks &b = idle_blocks();
+      std::lock_guard<std::mutex> g(b.mu);
+      b.size.erase(*p);
+    }
+    CK(cudaFreeAsync(*p, s));
+  }
+  *p = dev_take(bytes, s);
 }
 
 static void require_device() {
@@ -1601,11 +1669,11 @@ struct tsl_engine {
     // (dev_grow keeps its freed memory cached): a fresh engine reuses the
     // previous one's memory, and its teardown never synchronises the device
     pool_keep();
-    CK(cudaMallocAsync((void **)&d_pool, pool.size() * sizeof(int), stream));
+    d_pool = (int *)dev_take(pool.size() * sizeof(int), stream);
     h2d(d_pool, pool.data(), pool.size() * sizeof(int), stream);
     CK(cudaStreamSynchronize(stream));
-    CK(cudaMallocAsync((void **)&d_counters, 8 * sizeof(int), stream));  // [4] = speculative retirement limit
-    CK(cudaMallocAsync((void **)&d_stats, 8 * sizeof(unsigned long long), stream));
+    d_counters = (int *)dev_take(8 * sizeof(int), stream);  // [4] = speculative retirement limit
+    d_stats = (unsigned long long *)dev_take(8 * sizeof(unsigned long long), stream);
     smem_bytes = pool.size() * sizeof(int);
     if (smem_bytes > 48 * 1024) {
       CK(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1621,7 +1689,7 @@ struct tsl_engine {
     (void)ndep;
     ws_words = rep_ws_words(pool.data());
     ws_threads = num_sms * 4 * 128;
-    CK(cudaMallocAsync((void **)&d_ws, (size_t)ws_threads * ws_words * sizeof(int), stream));
+    d_ws = (int *)dev_take((size_t)ws_threads * ws_words * sizeof(int), stream);
     CK(cudaStreamSynchronize(stream));
     gpu_ready = true;
   }
@@ -1660,20 +1728,26 @@ struct tsl_engine {
 
   ~tsl_engine() {
     if (!gpu_ready) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);  // blocks are parked under the engine's device
     // stream-ordered frees back into the pool, after the work queued on the
     // engine's streams (a synchronous cudaFree stalled a caller's next
     // search by up to 0.5 s); stream and event destruction do not block
+    // the engine's own streams finish first (normally already idle): its
+    // buffers are then parked for the next engine (dev_park)
+    for (auto &vs : vslot) cudaStreamSynchronize(vs.st);
+    cudaStreamSynchronize(stream);
     for (auto &vs : vslot) {
-      cudaStreamWaitEvent(stream, vs.ev1, 0);
-      if (vs.rows) cudaFreeAsync(vs.rows, vs.st);
-      if (vs.buf) cudaFreeAsync(vs.buf, vs.st);
+      dev_park(vs.rows, stream);
+      dev_park(vs.buf, stream);
     }
     for (void *p : {(void *)d_pool, (void *)d_cnt, (void *)d_off, (void *)d_assign, (void *)d_gate,
                     (void *)d_act[0], (void *)d_act[1], (void *)d_sat_widx, (void *)d_sat_starts,
                     (void *)d_counters, (void *)d_stats, (void *)d_ws, (void *)d_gather,
                     (void *)d_def[0], (void *)d_def[1], (void *)d_verify, (void *)d_surv,
                     (void *)d_sat_key, (void *)d_sat_next, (void *)d_stash_idx})
-      if (p) cudaFreeAsync(p, stream);
+      dev_park(p, stream);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     cudaEventDestroy(evm);
@@ -1684,6 +1758,7 @@ struct tsl_engine {
       cudaStreamDestroy(vs.st);
     }
     cudaStreamDestroy(stream);
+    cudaSetDevice(prev);
   }
 };
 
@@ -2338,8 +2413,8 @@ int tsl_engine_sat_next(tsl_engine *e, int64_t after, int64_t *widx_out, int32_t
   *widx_out = -1;
   if (e->n_sat <= 0) return TSL_OK;
   if (!e->d_sat_key) {
-    CK(cudaMallocAsync((void **)&e->d_sat_key, sizeof(unsigned long long), e->stream));
-    CK(cudaMallocAsync((void **)&e->d_sat_next, (size_t)(K + 1) * sizeof(int), e->stream));
+    e->d_sat_key = (unsigned long long *)dev_take(sizeof(unsigned long long), e->stream);
+    e->d_sat_next = (int *)dev_take((size_t)(K + 1) * sizeof(int), e->stream);
   }
   CK(cudaMemsetAsync(e->d_sat_key, 0xff, sizeof(unsigned long long), e->stream));
   const long long n = e->n_sat;
